@@ -1,0 +1,110 @@
+"""Oracle: task generation + H_eff·ψ on the compact plan form (numpy).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Restates
+  * blocks.py:503-579  build_plan   — row x ψ-key matching, scale folding,
+    grouping by (ψ key, out key), members in table-row order;
+  * dmrg.py:107-176    apply_plan   — per group: stage L/R stacks (R scaled,
+    dmrg.py:136-140), then sbmm4s's two kernels (sbmm4s.py:127-157).
+"""
+
+import numpy as np
+
+from .sbmm4s import batched_gemm_interleaved, concat_gemm_accumulate
+
+
+def psi_layout(pi):
+    """(keys, offsets) of the ψ vector — blocks.py:416-429 and :448."""
+    keys = pi.psi_keys()
+    return keys, pi.psi_offsets(keys)
+
+
+def build_groups(pi):
+    """Reference grouping restated on the compact form (blocks.py:521-567).
+
+    Returns a list of (psi index, out index, [(row, scale), ...]) in sorted
+    (ψ key, out key) order; members in row order.
+    """
+    keys, _ = psi_layout(pi)
+    index = {k[:3]: i for i, k in enumerate(keys)}
+    qn_l = [tuple(q) for q in pi.qn_l.tolist()]
+    qn_r = [tuple(q) for q in pi.qn_r.tolist()]
+    lidx = {q: j for j, q in enumerate(qn_l)}
+    ridx = {q: j for j, q in enumerate(qn_r)}
+
+    def shifted(idx, qns, j, delta):
+        return idx.get(tuple(a + b for a, b in zip(qns[j], delta)), -1)
+
+    groups = {}
+    for t in range(pi.nrows):                                   # blocks.py:521
+        lo, ro = int(pi.lop[t]), int(pi.rop[t])
+        dl, dr = pi.delta_l[lo].tolist(), pi.delta_r[ro].tolist()
+        for i, (jl, s1, s2, jr) in enumerate(keys):               # blocks.py:535
+            d1 = int(pi.site1_dst[t, s1])
+            d2 = int(pi.site2_dst[t, s2])
+            if d1 < 0 or d2 < 0:                                  # blocks.py:539
+                continue
+            jlp = shifted(lidx, qn_l, jl, dl)                     # blocks.py:543
+            if jlp < 0 or pi.blk_off_l[lo, jl] < 0:
+                continue
+            jrp = shifted(ridx, qn_r, jr, dr)                     # blocks.py:547
+            if jrp < 0 or pi.blk_off_r[ro, jr] < 0:
+                continue
+            o = index.get((jlp, d1, d2), -1)                      # blocks.py:551
+            if o < 0 or keys[o][3] != jrp:
+                continue
+            scale = float(pi.alpha[t]) * float(pi.site1_val[t, s1]) * float(pi.site2_val[t, s2])
+            if pi.e_l[t]:                                         # blocks.py:555
+                scale *= float(pi.left_sign[jl])
+            if scale == 0.0:                                      # blocks.py:561
+                continue
+            groups.setdefault((i, o), []).append((t, scale))
+    return [(i, o, groups[(i, o)]) for (i, o) in sorted(groups)]
+
+
+def _block(arena, off, rows, cols):
+    return arena[off:off + rows * cols].reshape(rows, cols)
+
+
+def apply_groups(pi, groups, psi, out=None):
+    """out += H_eff psi, group by group, sbmm4s two-step (dmrg.py:120-163)."""
+    keys, offs = psi_layout(pi)
+    out = np.zeros_like(psi) if out is None else out
+    for i, o, members in groups:
+        jl, _s1, _s2, jr = keys[i]
+        m, n = int(pi.dim_l[jl]), int(pi.dim_r[jr])
+        ojl, ojr = keys[o][0], keys[o][3]
+        q, r = int(pi.dim_l[ojl]), int(pi.dim_r[ojr])
+        a = psi[offs[i]:offs[i] + m * n].reshape(m, n)
+        b = out[offs[o]:offs[o] + q * r].reshape(q, r)
+        p = len(members)
+        l_stack = np.empty((q, m, p), order="F")                  # dmrg.py:130
+        r_stack = np.empty((r, n, p), order="F")                  # dmrg.py:136
+        for k, (t, s) in enumerate(members):
+            lo, ro = int(pi.lop[t]), int(pi.rop[t])
+            l_stack[:, :, k] = _block(pi.arena_l, int(pi.blk_off_l[lo, jl]), q, m)
+            np.multiply(_block(pi.arena_r, int(pi.blk_off_r[ro, jr]), r, n), s,
+                        out=r_stack[:, :, k])
+        ws = np.zeros(m * p * r)
+        temp = batched_gemm_interleaved(a, r_stack, ws)           # dmrg.py:152
+        concat_gemm_accumulate(l_stack, temp, 1.0, b)             # dmrg.py:156
+    return out
+
+
+def apply_heff(pi, psi, groups=None):
+    """H_eff psi from scratch (zeroed output), the Lanczos apply_op."""
+    groups = build_groups(pi) if groups is None else groups
+    return apply_groups(pi, groups, psi)
+
+
+def ref_flops(pi, groups):
+    """plan.flops — sbmm4s.py:205 flops_fused summed over groups (blocks.py:571)."""
+    keys, _ = psi_layout(pi)
+    total = 0
+    for i, o, members in groups:
+        m, n = int(pi.dim_l[keys[i][0]]), int(pi.dim_r[keys[i][3]])
+        q, r = int(pi.dim_l[keys[o][0]]), int(pi.dim_r[keys[o][3]])
+        p = len(members)
+        total += 2 * m * r * n * p + 2 * q * r * m * p
+    return total

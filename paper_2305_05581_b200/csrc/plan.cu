@@ -1,0 +1,539 @@
+// plan.cu — task generation and execution of H_eff·ψ (blocks.py:503
+// build_plan + dmrg.py:107 apply_plan), the north star's items (1)-(3):
+//
+//  (1) block-sparse layout: operator blocks packed in one device arena per
+//      block side with an (op, column sector) -> offset index table; ψ/σ in
+//      the reference's to_vector layout (blocks.py:448).
+//  (2) task generation: every operator-table row is matched against every ψ
+//      sector (the reference's row x ψ-key double loop, blocks.py:521-565),
+//      producing the reference's (ψ key, out key) groups with per-member
+//      scales — bit-identical grouping, retained on request for parity.
+//  (3) the work list for the FP64 engine, in two phases per workspace chunk:
+//        phase 1   T(k, R) = A_k R^T           one GEMM per distinct (ψ key,
+//                                              right op) — shared by every
+//                                              member that uses it
+//        phase 2   σ[out] += Σ s_i L_i T_i     one problem per out key, its K
+//                                              the concatenation of members
+//      which is SBMM4S (sbmm4s.py Alg. 2) with the interleaved temp stack
+//      replaced by deduplicated T blocks and the member sum carried by the
+//      shared inner dimension (no reduction pass, no atomics).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <vector>
+
+#include "../../include/sdmrg_b200.h"
+#include "runtime.h"
+
+using namespace sdmrg;
+
+namespace {
+
+enum { B_PSI = 0, B_SIGMA = 1, B_ARENA_L = 2, B_ARENA_R = 3, B_WS = 4 };
+
+struct Member {
+  int32_t out;
+  int32_t row;
+  double scale;
+};
+
+struct Chunk {
+  GemmBatch host1, host2;  // released after upload
+  DeviceBatch p1, p2;
+  int64_t ws_doubles = 0;
+  int64_t flops1 = 0, flops2 = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+}  // namespace
+
+struct sdmrg_plan {
+  int ncomp = 0, nsite = 0, nL = 0, nR = 0;
+  std::vector<int32_t> keys;     // psi_keys x 4 (jl, s1, s2, jr)
+  std::vector<int64_t> offs;     // psi_keys + 1
+  // reference grouping (optional)
+  std::vector<int32_t> g_psi, g_out;
+  std::vector<int64_t> g_begin;
+  std::vector<int32_t> m_row;
+  std::vector<double> m_scale;
+  std::vector<Chunk> chunks;
+  double* workspace = nullptr;
+  int* counters = nullptr;
+  const double* arena_l = nullptr;
+  const double* arena_r = nullptr;
+  sdmrg_plan_stats stats{};
+  int timing = 0;
+};
+
+namespace {
+
+using QN = std::vector<int32_t>;
+
+QN qn_at(const int32_t* base, int i, int ncomp) { return QN(base + (int64_t)i * ncomp, base + (int64_t)(i + 1) * ncomp); }
+
+int validate(const sdmrg_plan_desc* d) {
+  if (!d) return fail(SDMRG_EINVAL, "plan: null descriptor");
+  if (d->ncomp <= 0 || d->nsite <= 0 || d->nsec_l <= 0 || d->nsec_r <= 0)
+    return fail(SDMRG_EINVAL, "plan: empty basis or bad QN width");
+  if (d->nrows < 0 || d->nops_l < 0 || d->nops_r < 0) return fail(SDMRG_EINVAL, "plan: negative count");
+  if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
+    return fail(SDMRG_EINVAL, "plan: bad rank/world");
+  for (int64_t t = 0; t < d->nrows; ++t) {
+    if (d->lop[t] < 0 || d->lop[t] >= d->nops_l || d->rop[t] < 0 || d->rop[t] >= d->nops_r)
+      return fail(SDMRG_EINVAL, "plan: row references a missing operator");
+    for (int s = 0; s < d->nsite; ++s) {
+      if (d->site1_dst[t * d->nsite + s] >= d->nsite || d->site2_dst[t * d->nsite + s] >= d->nsite)
+        return fail(SDMRG_EINVAL, "plan: site map out of range");
+    }
+  }
+  for (int j = 0; j < d->nsec_l; ++j)
+    if (d->dim_l[j] <= 0) return fail(SDMRG_EINVAL, "plan: non-positive left sector dim");
+  for (int j = 0; j < d->nsec_r; ++j)
+    if (d->dim_r[j] <= 0) return fail(SDMRG_EINVAL, "plan: non-positive right sector dim");
+  return SDMRG_OK;
+}
+
+// shift[o * nsec + j] = index of qn[j] + delta[o] in the basis, or -1
+std::vector<int32_t> shift_table(int nops, const int32_t* delta, int nsec, const int32_t* qn,
+                                 int ncomp) {
+  std::map<QN, int> index;
+  for (int j = 0; j < nsec; ++j) index[qn_at(qn, j, ncomp)] = j;
+  std::vector<int32_t> out((size_t)nops * nsec, -1);
+  std::map<QN, std::vector<int32_t>> memo;
+  for (int o = 0; o < nops; ++o) {
+    QN dq = qn_at(delta, o, ncomp);
+    auto it = memo.find(dq);
+    if (it == memo.end()) {
+      std::vector<int32_t> row(nsec, -1);
+      for (int j = 0; j < nsec; ++j) {
+        QN q = qn_at(qn, j, ncomp);
+        for (int c = 0; c < ncomp; ++c) q[c] += dq[c];
+        auto f = index.find(q);
+        if (f != index.end()) row[j] = f->second;
+      }
+      it = memo.emplace(dq, row).first;
+    }
+    std::copy(it->second.begin(), it->second.end(), out.begin() + (size_t)o * nsec);
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
+  if (!out) return fail(SDMRG_EINVAL, "plan: null output");
+  *out = nullptr;
+  int rc = validate(d);
+  if (rc) return rc;
+  const int nc = d->ncomp, ns = d->nsite, nL = d->nsec_l, nR = d->nsec_r;
+  auto* plan = new sdmrg_plan();
+  plan->ncomp = nc;
+  plan->nsite = ns;
+  plan->nL = nL;
+  plan->nR = nR;
+  plan->arena_l = d->arena_l;
+  plan->arena_r = d->arena_r;
+
+  // ---- ψ keys (blocks.py:416-429): qR = target - qL - q1 - q2 ∈ right basis
+  std::map<QN, int> rindex;
+  for (int j = 0; j < nR; ++j) rindex[qn_at(d->qn_r, j, nc)] = j;
+  struct Key {
+    int32_t jl, s1, s2, jr;
+  };
+  std::vector<Key> keys;
+  for (int jl = 0; jl < nL; ++jl)
+    for (int s1 = 0; s1 < ns; ++s1)
+      for (int s2 = 0; s2 < ns; ++s2) {
+        QN q(nc);
+        for (int c = 0; c < nc; ++c)
+          q[c] = d->target[c] - d->qn_l[jl * nc + c] - d->site_qn[s1 * nc + c] - d->site_qn[s2 * nc + c];
+        auto f = rindex.find(q);
+        if (f != rindex.end()) keys.push_back({jl, s1, s2, f->second});
+      }
+  auto key_qns = [&](const Key& k) {
+    QN v;
+    v.reserve(4 * nc);
+    for (int c = 0; c < nc; ++c) v.push_back(d->qn_l[k.jl * nc + c]);
+    for (int c = 0; c < nc; ++c) v.push_back(d->site_qn[k.s1 * nc + c]);
+    for (int c = 0; c < nc; ++c) v.push_back(d->site_qn[k.s2 * nc + c]);
+    for (int c = 0; c < nc; ++c) v.push_back(d->qn_r[k.jr * nc + c]);
+    return v;
+  };
+  std::stable_sort(keys.begin(), keys.end(),
+                   [&](const Key& a, const Key& b) { return key_qns(a) < key_qns(b); });
+  const int64_t nk = static_cast<int64_t>(keys.size());
+  plan->keys.resize(nk * 4);
+  plan->offs.resize(nk + 1);
+  std::vector<int32_t> psi_index((size_t)nL * ns * ns, -1);
+  int64_t off = 0;
+  for (int64_t i = 0; i < nk; ++i) {
+    const Key& k = keys[i];
+    plan->keys[i * 4 + 0] = k.jl;
+    plan->keys[i * 4 + 1] = k.s1;
+    plan->keys[i * 4 + 2] = k.s2;
+    plan->keys[i * 4 + 3] = k.jr;
+    plan->offs[i] = off;
+    off += (int64_t)d->dim_l[k.jl] * d->dim_r[k.jr];
+    psi_index[((size_t)k.jl * ns + k.s1) * ns + k.s2] = static_cast<int32_t>(i);
+  }
+  plan->offs[nk] = off;
+
+  const std::vector<int32_t> shL = shift_table(d->nops_l, d->delta_l, nL, d->qn_l, nc);
+  const std::vector<int32_t> shR = shift_table(d->nops_r, d->delta_r, nR, d->qn_r, nc);
+
+  // ---- task generation: members per ψ key, rows in table order
+  std::vector<std::vector<Member>> per_key(nk);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t i = 0; i < nk; ++i) {
+    const Key& k = keys[i];
+    std::vector<Member>& mem = per_key[i];
+    for (int64_t t = 0; t < d->nrows; ++t) {
+      const int d1 = d->site1_dst[t * ns + k.s1];
+      if (d1 < 0) continue;
+      const int d2 = d->site2_dst[t * ns + k.s2];
+      if (d2 < 0) continue;
+      const int lo = d->lop[t], ro = d->rop[t];
+      const int jlp = shL[(size_t)lo * nL + k.jl];
+      if (jlp < 0 || d->blk_off_l[(int64_t)lo * nL + k.jl] < 0) continue;
+      const int jrp = shR[(size_t)ro * nR + k.jr];
+      if (jrp < 0 || d->blk_off_r[(int64_t)ro * nR + k.jr] < 0) continue;
+      const int o = psi_index[((size_t)jlp * ns + d1) * ns + d2];
+      if (o < 0 || keys[o].jr != jrp) continue;
+      double scale = d->alpha[t] * d->site1_val[t * ns + k.s1] * d->site2_val[t * ns + k.s2];
+      if (d->e_l[t]) scale *= d->left_sign[k.jl];
+      if (scale == 0.0) continue;
+      mem.push_back({o, static_cast<int32_t>(t), scale});
+    }
+    std::stable_sort(mem.begin(), mem.end(),
+                     [](const Member& a, const Member& b) { return a.out < b.out; });
+  }
+
+  // ---- statistics in the reference's FLOP convention (sbmm4s.py:205)
+  int64_t groups = 0, members = 0, ref_flops = 0;
+  std::vector<double> key_cost(nk, 0.0);
+  for (int64_t i = 0; i < nk; ++i) {
+    const auto& mem = per_key[i];
+    const int64_t m = d->dim_l[keys[i].jl], n = d->dim_r[keys[i].jr];
+    members += (int64_t)mem.size();
+    for (size_t a = 0; a < mem.size();) {
+      size_t b = a;
+      while (b < mem.size() && mem[b].out == mem[a].out) ++b;
+      const int64_t p = (int64_t)(b - a);
+      const int64_t q = d->dim_l[keys[mem[a].out].jl], r = d->dim_r[keys[mem[a].out].jr];
+      ref_flops += 2 * m * r * n * p + 2 * q * r * m * p;
+      key_cost[i] += double(2 * q * r * m * p);
+      ++groups;
+      a = b;
+    }
+  }
+  if (d->keep_groups) {
+    plan->g_begin.push_back(0);
+    for (int64_t i = 0; i < nk; ++i) {
+      const auto& mem = per_key[i];
+      for (size_t a = 0; a < mem.size();) {
+        size_t b = a;
+        while (b < mem.size() && mem[b].out == mem[a].out) ++b;
+        plan->g_psi.push_back(static_cast<int32_t>(i));
+        plan->g_out.push_back(mem[a].out);
+        for (size_t c = a; c < b; ++c) {
+          plan->m_row.push_back(mem[c].row);
+          plan->m_scale.push_back(mem[c].scale);
+        }
+        plan->g_begin.push_back(static_cast<int64_t>(plan->m_row.size()));
+        a = b;
+      }
+    }
+  }
+
+  // ---- shard ψ keys over ranks (greedy LPT on phase-2 cost, deterministic)
+  std::vector<char> mine(nk, 1);
+  if (d->world > 1) {
+    std::vector<int64_t> order(nk);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t a, int64_t b) { return key_cost[a] > key_cost[b]; });
+    std::vector<double> load(d->world, 0.0);
+    for (int64_t idx : order) {
+      int best = 0;
+      for (int w = 1; w < d->world; ++w)
+        if (load[w] < load[best]) best = w;
+      load[best] += key_cost[idx] + 1.0;
+      mine[idx] = (best == d->rank);
+    }
+  }
+
+  // ---- execution schedule: chunks of ψ keys bounded by T workspace
+  std::vector<int64_t> t_need(nk, 0);  // doubles of distinct non-identity T per key
+  std::vector<std::vector<std::pair<int32_t, int64_t>>> t_slots(nk);  // (rop, ws offset|-1)
+  for (int64_t i = 0; i < nk; ++i) {
+    if (!mine[i]) continue;
+    const int64_t m = d->dim_l[keys[i].jl];
+    std::vector<int32_t> rops;
+    for (const Member& mb : per_key[i]) rops.push_back(d->rop[mb.row]);
+    std::sort(rops.begin(), rops.end());
+    rops.erase(std::unique(rops.begin(), rops.end()), rops.end());
+    for (int32_t ro : rops) {
+      if (d->kind_r[ro] == 1) continue;
+      const int jrp = shR[(size_t)ro * nR + keys[i].jr];
+      t_need[i] += m * d->dim_r[jrp];
+    }
+  }
+  int64_t total_t = 0;
+  for (int64_t i = 0; i < nk; ++i) total_t += t_need[i];
+  int64_t budget = d->workspace_doubles;
+  if (budget <= 0 && !d->dry_run) {
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    budget = std::max<int64_t>(1 << 20, (int64_t)(free_b / 8 * 0.30));
+  }
+  int64_t max_key = 0;
+  for (int64_t i = 0; i < nk; ++i) max_key = std::max(max_key, t_need[i]);
+  budget = std::max(budget, max_key);
+  budget = std::min(budget, std::max<int64_t>(total_t, 1));
+
+  int64_t exec_flops = 0, local_members = 0, t_problems = 0, tiles = 0, segments = 0;
+  double algo_bytes = 16.0 * off;
+  {
+    // unique operator blocks touched (compulsory reads)
+    std::vector<char> seen_l((size_t)d->nops_l * nL, 0), seen_r((size_t)d->nops_r * nR, 0);
+    for (int64_t i = 0; i < nk; ++i) {
+      if (!mine[i]) continue;
+      for (const Member& mb : per_key[i]) {
+        const int lo = d->lop[mb.row], ro = d->rop[mb.row];
+        char& sl = seen_l[(size_t)lo * nL + keys[i].jl];
+        if (!sl) {
+          sl = 1;
+          algo_bytes += 8.0 * d->dim_l[keys[i].jl] * d->dim_l[shL[(size_t)lo * nL + keys[i].jl]];
+        }
+        char& sr = seen_r[(size_t)ro * nR + keys[i].jr];
+        if (!sr) {
+          sr = 1;
+          algo_bytes += 8.0 * d->dim_r[keys[i].jr] * d->dim_r[shR[(size_t)ro * nR + keys[i].jr]];
+        }
+      }
+    }
+  }
+
+  int64_t i0 = d->dry_run ? nk : 0;  // dry run: task generation + stats only
+  while (i0 < nk) {
+    Chunk ch;
+    int64_t used = 0, i1 = i0;
+    while (i1 < nk && (i1 == i0 || used + t_need[i1] <= budget)) {
+      used += t_need[i1];
+      ++i1;
+    }
+    // phase 1: distinct T per (key, right op)
+    std::vector<std::map<int32_t, std::pair<uint64_t, int>>> tmap(i1 - i0);  // rop -> (handle, ld)
+    int64_t ws = 0;
+    for (int64_t i = i0; i < i1; ++i) {
+      if (!mine[i]) continue;
+      const Key& k = keys[i];
+      const int m = d->dim_l[k.jl], n = d->dim_r[k.jr];
+      for (const Member& mb : per_key[i]) {
+        const int ro = d->rop[mb.row];
+        auto& tm = tmap[i - i0];
+        if (tm.count(ro)) continue;
+        if (d->kind_r[ro] == 1) {  // R = identity: T = A (no product)
+          tm[ro] = {make_handle(B_PSI, plan->offs[i]), n};
+          continue;
+        }
+        const int jrp = shR[(size_t)ro * nR + k.jr];
+        const int r = d->dim_r[jrp];
+        tm[ro] = {make_handle(B_WS, ws), r};
+        ch.host1.begin_prob(make_handle(B_WS, ws), r, m, r, 0);
+        ch.host1.add_seg(make_handle(B_PSI, plan->offs[i]), n,
+                         make_handle(B_ARENA_R, d->blk_off_r[(int64_t)ro * nR + k.jr]), n, n, 1.0);
+        ch.host1.end_prob();
+        ws += (int64_t)m * r;
+        exec_flops += 2LL * m * n * r;
+        ch.flops1 += 2LL * m * n * r;
+        ++t_problems;
+      }
+    }
+    // phase 2: one problem per out key, segments ordered (ψ key, row)
+    std::map<int32_t, std::vector<std::pair<int64_t, const Member*>>> by_out;
+    for (int64_t i = i0; i < i1; ++i) {
+      if (!mine[i]) continue;
+      for (const Member& mb : per_key[i]) by_out[mb.out].push_back({i, &mb});
+    }
+    for (auto& kv : by_out) {
+      const int32_t o = kv.first;
+      const int q = d->dim_l[keys[o].jl], r = d->dim_r[keys[o].jr];
+      ch.host2.begin_prob(make_handle(B_SIGMA, plan->offs[o]), r, q, r, 1);
+      for (auto& e : kv.second) {
+        const int64_t i = e.first;
+        const Member& mb = *e.second;
+        const int m = d->dim_l[keys[i].jl];
+        const int lo = d->lop[mb.row], ro = d->rop[mb.row];
+        const auto& th = tmap[i - i0].at(ro);
+        ch.host2.add_seg(make_handle(B_ARENA_L, d->blk_off_l[(int64_t)lo * nL + keys[i].jl]), m,
+                         th.first, th.second, m, mb.scale);
+        exec_flops += 2LL * q * r * m;
+        ch.flops2 += 2LL * q * r * m;
+        ++local_members;
+      }
+      ch.host2.end_prob();
+    }
+    ch.host1.finalize_tiles();
+    ch.host2.finalize_tiles();
+    ch.ws_doubles = ws;
+    tiles += (int64_t)(ch.host1.tiles.size() + ch.host2.tiles.size());
+    segments += (int64_t)(ch.host1.segs.size() + ch.host2.segs.size());
+    plan->chunks.push_back(std::move(ch));
+    i0 = i1;
+  }
+
+  int64_t ws_max = 0;
+  for (auto& ch : plan->chunks) ws_max = std::max(ws_max, ch.ws_doubles);
+  rc = SDMRG_OK;
+  if (ws_max > 0) rc = cuda_check(cudaMalloc(&plan->workspace, sizeof(double) * ws_max), "cudaMalloc workspace");
+  if (!rc && !plan->chunks.empty())
+    rc = cuda_check(cudaMalloc(&plan->counters, sizeof(int) * 2 * plan->chunks.size()),
+                    "cudaMalloc counters");
+  for (auto& ch : plan->chunks) {
+    if (rc) break;
+    rc = ch.host1.upload(&ch.p1, 0);
+    if (!rc) rc = ch.host2.upload(&ch.p2, 0);
+    ch.host1 = GemmBatch();
+    ch.host2 = GemmBatch();
+  }
+  if (rc) {
+    sdmrg_plan_destroy(plan);
+    return rc;
+  }
+  sdmrg_plan_stats& st = plan->stats;
+  st.psi_keys = nk;
+  st.psi_size = off;
+  st.groups = groups;
+  st.members = members;
+  st.ref_flops = ref_flops;
+  st.exec_flops = exec_flops;
+  st.local_members = local_members;
+  st.t_problems = t_problems;
+  st.tiles = tiles;
+  st.segments = segments;
+  st.chunks = static_cast<int64_t>(plan->chunks.size());
+  st.workspace_doubles = ws_max;
+  int64_t kernels = 0;
+  for (auto& ch : plan->chunks) kernels += (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0);
+  st.kernels_per_apply = kernels;
+  st.algo_bytes = static_cast<int64_t>(algo_bytes);
+  *out = plan;
+  return SDMRG_OK;
+}
+
+int sdmrg_plan_stats_get(const sdmrg_plan* plan, sdmrg_plan_stats* out) {
+  if (!plan || !out) return fail(SDMRG_EINVAL, "plan_stats: null argument");
+  *out = plan->stats;
+  return SDMRG_OK;
+}
+
+int sdmrg_plan_layout(const sdmrg_plan* plan, int32_t* keys, int64_t* offsets) {
+  if (!plan) return fail(SDMRG_EINVAL, "plan_layout: null plan");
+  if (keys) std::memcpy(keys, plan->keys.data(), plan->keys.size() * sizeof(int32_t));
+  if (offsets) std::memcpy(offsets, plan->offs.data(), plan->offs.size() * sizeof(int64_t));
+  return SDMRG_OK;
+}
+
+int sdmrg_plan_groups(const sdmrg_plan* plan, int32_t* group_psi, int32_t* group_out,
+                      int64_t* group_begin, int64_t* member_row, double* member_scale) {
+  if (!plan) return fail(SDMRG_EINVAL, "plan_groups: null plan");
+  if (plan->g_begin.empty()) return fail(SDMRG_EINVAL, "plan_groups: built without keep_groups");
+  std::copy(plan->g_psi.begin(), plan->g_psi.end(), group_psi);
+  std::copy(plan->g_out.begin(), plan->g_out.end(), group_out);
+  std::copy(plan->g_begin.begin(), plan->g_begin.end(), group_begin);
+  for (size_t i = 0; i < plan->m_row.size(); ++i) member_row[i] = plan->m_row[i];
+  std::copy(plan->m_scale.begin(), plan->m_scale.end(), member_scale);
+  return SDMRG_OK;
+}
+
+int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int accumulate,
+                     void* stream_) {
+  if (!plan || !psi || !sigma) return fail(SDMRG_EINVAL, "plan_apply: null argument");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  int rc;
+  if (!accumulate && plan->stats.psi_size > 0) {
+    rc = cuda_check(cudaMemsetAsync(sigma, 0, sizeof(double) * plan->stats.psi_size, stream),
+                    "memset sigma");
+    if (rc) return rc;
+  }
+  if (plan->chunks.empty()) return SDMRG_OK;
+  rc = cuda_check(cudaMemsetAsync(plan->counters, 0, sizeof(int) * 2 * plan->chunks.size(), stream),
+                  "memset counters");
+  if (rc) return rc;
+  Bases bases{};
+  bases.p[B_PSI] = const_cast<double*>(psi);
+  bases.p[B_SIGMA] = sigma;
+  bases.p[B_ARENA_L] = const_cast<double*>(plan->arena_l);
+  bases.p[B_ARENA_R] = const_cast<double*>(plan->arena_r);
+  bases.p[B_WS] = plan->workspace;
+  for (size_t c = 0; c < plan->chunks.size(); ++c) {
+    Chunk& ch = plan->chunks[c];
+    if (plan->timing) cudaEventRecord(ch.ev[0], stream);
+    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 2 * c, stream);
+    if (rc) return rc;
+    if (plan->timing) {
+      cudaEventRecord(ch.ev[1], stream);
+      cudaEventRecord(ch.ev[2], stream);
+    }
+    rc = launch_engine(false, false, ch.p2, bases, plan->counters + 2 * c + 1, stream);
+    if (rc) return rc;
+    if (plan->timing) cudaEventRecord(ch.ev[3], stream);
+  }
+  return SDMRG_OK;
+}
+
+int sdmrg_plan_set_timing(sdmrg_plan* plan, int enable) {
+  if (!plan) return fail(SDMRG_EINVAL, "plan_set_timing: null plan");
+  if (enable && !plan->timing) {
+    for (auto& ch : plan->chunks)
+      for (auto& e : ch.ev) {
+        int rc = cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        if (rc) return rc;
+      }
+  }
+  plan->timing = enable ? 1 : 0;
+  return SDMRG_OK;
+}
+
+int sdmrg_plan_timing(sdmrg_plan* plan, double* ms1, double* ms2, int64_t* f1, int64_t* f2) {
+  if (!plan || !plan->timing) return fail(SDMRG_EINVAL, "plan_timing: timing not enabled");
+  double t1 = 0.0, t2 = 0.0;
+  int64_t a = 0, b = 0;
+  for (auto& ch : plan->chunks) {
+    int rc = cuda_check(cudaEventSynchronize(ch.ev[3]), "timing sync");
+    if (rc) return rc;
+    float x = 0.f, y = 0.f;
+    cudaEventElapsedTime(&x, ch.ev[0], ch.ev[1]);
+    cudaEventElapsedTime(&y, ch.ev[2], ch.ev[3]);
+    t1 += x;
+    t2 += y;
+    a += ch.flops1;
+    b += ch.flops2;
+  }
+  if (ms1) *ms1 = t1;
+  if (ms2) *ms2 = t2;
+  if (f1) *f1 = a;
+  if (f2) *f2 = b;
+  return SDMRG_OK;
+}
+
+int sdmrg_plan_destroy(sdmrg_plan* plan) {
+  if (!plan) return SDMRG_OK;
+  for (auto& ch : plan->chunks) {
+    ch.p1.release();
+    ch.p2.release();
+    for (auto& e : ch.ev)
+      if (e) cudaEventDestroy(e);
+  }
+  if (plan->workspace) cudaFree(plan->workspace);
+  if (plan->counters) cudaFree(plan->counters);
+  delete plan;
+  return SDMRG_OK;
+}
+
+}  // extern "C"

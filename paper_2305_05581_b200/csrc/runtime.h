@@ -1,0 +1,51 @@
+// runtime.h — host-side plumbing shared by the C-ABI entry points: error
+// slot, launch accounting, and GemmBatch (host staging of a grouped GEMM
+// descriptor list that is uploaded once and launched on the engine).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "engine.cuh"
+
+namespace sdmrg {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_check(cudaError_t e, const char* what);
+void count_launch(int n = 1);
+
+// Persistent-grid size for the engine (148 SMs x resident CTAs).
+int engine_grid(bool ta, bool tb);
+
+// Device-side copy of a descriptor list.
+struct DeviceBatch {
+  Tile* tiles = nullptr;
+  Prob* probs = nullptr;
+  Seg* segs = nullptr;
+  int64_t ntiles = 0, nprobs = 0, nsegs = 0;
+  void release();
+};
+
+// Host staging of problems/segments; tiles derived per problem.
+struct GemmBatch {
+  std::vector<Prob> probs;
+  std::vector<Seg> segs;
+  std::vector<Tile> tiles;
+  std::vector<double> tile_cost;
+  int begin_prob(uint64_t c, int ldc, int m, int n, int beta);
+  void add_seg(uint64_t a, int lda, uint64_t b, int ldb, int k, double scale);
+  void end_prob();
+  // order tiles by descending cost (longest-processing-time first)
+  void finalize_tiles();
+  int upload(DeviceBatch* out, cudaStream_t stream) const;
+  int64_t flops() const;  // useful (unpadded) FLOPs
+};
+
+// Launch the engine over an uploaded batch.  counter must point at one
+// zeroed device int (reset by the caller or by this function when reset=1).
+int launch_engine(bool ta, bool tb, const DeviceBatch& b, const Bases& bases, int* counter,
+                  cudaStream_t stream);
+
+}  // namespace sdmrg
