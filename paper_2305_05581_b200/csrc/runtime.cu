@@ -71,6 +71,7 @@ int GemmBatch::begin_prob(uint64_t c, int ldc, int m, int n, int beta) {
 }
 
 void GemmBatch::add_seg(uint64_t a, int lda, uint64_t b, int ldb, int k, double scale) {
+  if (k <= 0) return;  // the engine requires non-empty segments
   Seg s{};
   s.a = a;
   s.b = b;
