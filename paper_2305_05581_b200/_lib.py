@@ -98,7 +98,7 @@ EXPORTED = tuple(_SIGS)
 
 
 def lib_path():
-    return _build.LIB
+    return os.environ.get("SDMRG_LIB") or _build.LIB
 
 
 def load(rebuild=True):
@@ -108,7 +108,7 @@ def load(rebuild=True):
         if _lib is not None:
             return _lib
         path = lib_path()
-        if rebuild:
+        if rebuild and not os.environ.get("SDMRG_LIB"):
             try:
                 if _build.needs_build():
                     _build.build()

@@ -33,9 +33,9 @@ static int grid_for() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(seg_gemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
+                         smem_bytes<TA, TB>());
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, seg_gemm_kernel<TA, TB>, THREADS,
-                                                  SMEM_BYTES);
+                                                  smem_bytes<TA, TB>());
     grid = sms * std::max(per, 1);
   }
   return grid;
@@ -88,11 +88,19 @@ void GemmBatch::end_prob() {
   const Prob& p = probs[pi];
   int64_t ksum = 0;
   for (int s = p.seg_begin; s < p.seg_end; ++s) ksum += (segs[s].k + 3) / 4 * 4;
-  for (int r0 = 0; r0 < p.m; r0 += BM)
-    for (int c0 = 0; c0 < p.n; c0 += BN) {
-      Tile t{pi, r0, c0, 0};
+  // balanced tiles: ceil(extent/64) tiles per dimension of equal size
+  // (rounded up to the 8-row DMMA granularity), e.g. 138 -> 48+48+42
+  auto split = [](int extent, int cap) {
+    const int nt = (extent + cap - 1) / cap;
+    const int per = ((extent + nt - 1) / nt + 7) / 8 * 8;
+    return std::max(per, 8);
+  };
+  const int tm = split(p.m, BM), tn = split(p.n, BN);
+  for (int r0 = 0; r0 < p.m; r0 += tm)
+    for (int c0 = 0; c0 < p.n; c0 += tn) {
+      const int mm = std::min(tm, p.m - r0), nn = std::min(tn, p.n - c0);
+      Tile t{pi, r0, c0, static_cast<int16_t>(mm), static_cast<int16_t>(nn)};
       tiles.push_back(t);
-      const int mm = std::min(BM, p.m - r0), nn = std::min(BN, p.n - c0);
       tile_cost.push_back(double(ksum) * ((mm + 7) / 8 * 8) * ((nn + 7) / 8 * 8) + 4096.0);
     }
 }
@@ -156,7 +164,7 @@ int GemmBatch::upload(DeviceBatch* out, cudaStream_t stream) const {
 template <bool TA, bool TB>
 static void launch_t(const DeviceBatch& b, const Bases& bases, int* counter, cudaStream_t stream) {
   const int grid = std::min<int64_t>(grid_for<TA, TB>(), std::max<int64_t>(b.ntiles, 1));
-  seg_gemm_kernel<TA, TB><<<grid, THREADS, SMEM_BYTES, stream>>>(
+  seg_gemm_kernel<TA, TB><<<grid, THREADS, smem_bytes<TA, TB>(), stream>>>(
       b.tiles, static_cast<int>(b.ntiles), b.probs, b.segs, counter, bases);
 }
 
