@@ -9,10 +9,10 @@
  *
  * Entry point                     replaces (reference file:line)
  * ------------------------------  -------------------------------------------
- * sdmrg_dgemm                     gemm.py:56   NumpyGemm.gemm
- * sdmrg_dgemm_strided_batched     gemm.py:72   NumpyGemm.gemm_strided_batched
- * sdmrg_daxpy                     gemm.py:82   NumpyGemm.add_inplace
- * sdmrg_sbmm4s                    sbmm4s.py:165 sbmm4s (Alg. 2: two kernels,
+ * sdmrg_dgemm                     gemm.py:61   NumpyGemm.gemm
+ * sdmrg_dgemm_strided_batched     gemm.py:76   NumpyGemm.gemm_strided_batched
+ * sdmrg_daxpy                     gemm.py:86   NumpyGemm.add_inplace
+ * sdmrg_sbmm4s                    sbmm4s.py:167 sbmm4s (Alg. 2: two kernels,
  *                                 no reduction pass; chunked fallback :176)
  * sdmrg_plan_build                blocks.py:503 build_plan (task generation:
  *                                 operator-table rows x ψ sectors -> work list)
@@ -57,7 +57,7 @@ int sdmrg_dgemm(int transa, int transb, int m, int n, int k, double alpha,
                 const double* a, int lda, const double* b, int ldb,
                 double beta, double* c, int ldc, void* stream);
 
-/* c_i := op(a_i) @ op(b_i) for i < batch (one kernel; gemm.py:72 semantics:
+/* c_i := op(a_i) @ op(b_i) for i < batch (one kernel; gemm.py:76 semantics:
  * beta = 0, the members' outputs may interleave, e.g. ld = m*p, stride = m). */
 int sdmrg_dgemm_strided_batched(int transa, int transb, int m, int n, int k,
                                 const double* a, int lda, int64_t stride_a,
@@ -65,12 +65,12 @@ int sdmrg_dgemm_strided_batched(int transa, int transb, int m, int n, int k,
                                 double* c, int ldc, int64_t stride_c,
                                 int batch, void* stream);
 
-/* y += alpha * x (the lone standalone reduction kernel, gemm.py:82). */
+/* y += alpha * x (the lone standalone reduction kernel, gemm.py:86). */
 int sdmrg_daxpy(int64_t n, double alpha, const double* x, double* y,
                 void* stream);
 
 /* ---------------------------------------------------------------- SBMM4S --
- * B := B + alpha * sum_{i<p} L_i A R_i^T      (sbmm4s.py:165, Alg. 2)
+ * B := B + alpha * sum_{i<p} L_i A R_i^T      (sbmm4s.py:167, Alg. 2)
  * A: m x n (lda), B: q x r (ldb), L_i: q x m at l + i*stride_l (ldl),
  * R_i: r x n at r_stack + i*stride_r (ldr); all column-major device memory.
  * workspace: >= m*r doubles; with < m*p*r the batch is split in halves
@@ -166,6 +166,9 @@ typedef struct sdmrg_plan_stats {
   int64_t workspace_doubles;
   int64_t kernels_per_apply;
   int64_t algo_bytes;              /* algorithmic HBM bytes per apply         */
+  int64_t products;                /* phase-2 products (group, right op)      */
+  int64_t combine_outputs;         /* pre-summed left operators per apply     */
+  int64_t combine_terms;           /* their summands                          */
 } sdmrg_plan_stats;
 
 int sdmrg_plan_build(const sdmrg_plan_desc* desc, sdmrg_plan** out);
@@ -182,12 +185,12 @@ int sdmrg_plan_groups(const sdmrg_plan* plan, int32_t* group_psi,
 int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma,
                      int accumulate, void* stream);
 /* Per-launch CUDA-event timing of subsequent applies (bench instrumentation).
- * sdmrg_plan_timing syncs the last apply's events and writes the summed
- * device milliseconds of phase 1 (T = A R^T) and phase 2 (σ += L T) kernels
- * and the matching executed FLOPs.                                           */
+ * sdmrg_plan_timing syncs the last apply's events and writes, per phase
+ * (0: left-operator pre-summation, 1: T = A R^T, 2: σ += Lsum T), the summed
+ * device milliseconds ms[3], the executed FLOPs flops[3] and (phase 0 only)
+ * the algorithmic bytes bytes[3].  Any pointer may be NULL.                 */
 int sdmrg_plan_set_timing(sdmrg_plan* plan, int enable);
-int sdmrg_plan_timing(sdmrg_plan* plan, double* ms_phase1, double* ms_phase2,
-                      int64_t* flops_phase1, int64_t* flops_phase2);
+int sdmrg_plan_timing(sdmrg_plan* plan, double* ms, int64_t* flops, int64_t* bytes);
 int sdmrg_plan_destroy(sdmrg_plan* plan);
 
 /* ------------------------------------------------------- vector algebra --

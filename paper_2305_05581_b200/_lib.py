@@ -57,7 +57,8 @@ class PlanStats(ctypes.Structure):
     _fields_ = [(name, c_i64) for name in (
         "psi_keys", "psi_size", "groups", "members", "ref_flops", "exec_flops",
         "local_members", "t_problems", "tiles", "segments", "chunks",
-        "workspace_doubles", "kernels_per_apply", "algo_bytes")]
+        "workspace_doubles", "kernels_per_apply", "algo_bytes", "products",
+        "combine_outputs", "combine_terms")]
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
@@ -82,7 +83,7 @@ _SIGS = {
     "sdmrg_plan_apply": (c_int, [c_vp, c_vp, c_vp, c_int, c_vp]),
     "sdmrg_plan_destroy": (c_int, [c_vp]),
     "sdmrg_plan_set_timing": (c_int, [c_vp, c_int]),
-    "sdmrg_plan_timing": (c_int, [c_vp, P_dbl, P_dbl, P_i64, P_i64]),
+    "sdmrg_plan_timing": (c_int, [c_vp, P_dbl, P_i64, P_i64]),
     "sdmrg_dot": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),
     "sdmrg_nrm2": (c_int, [c_i64, c_vp, c_vp, c_vp]),
     "sdmrg_gemv_t": (c_int, [c_int, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),

@@ -12,8 +12,10 @@
 //        phase 1   T(k, R) = A_k R^T           one GEMM per distinct (ψ key,
 //                                              right op) — shared by every
 //                                              member that uses it
-//        phase 2   σ[out] += Σ s_i L_i T_i     one problem per out key, its K
-//                                              the concatenation of members
+//        phase 0   Lsum = Σ s_t L_t            per (group, right op) with >1
+//                                              member (combine.cuh)
+//        phase 2   σ[out] += Σ Lsum T          one problem per out key, its K
+//                                              the concatenation of products
 //      which is SBMM4S (sbmm4s.py Alg. 2) with the interleaved temp stack
 //      replaced by deduplicated T blocks and the member sum carried by the
 //      shared inner dimension (no reduction pass, no atomics).
@@ -25,6 +27,7 @@
 #include <vector>
 
 #include "../../include/sdmrg_b200.h"
+#include "combine.cuh"
 #include "runtime.h"
 
 using namespace sdmrg;
@@ -39,12 +42,31 @@ struct Member {
   double scale;
 };
 
+// One phase-2 product: (group (ψ key, out key), right op) with the member
+// left operators pre-summed (combine.cuh).
+struct Pair {
+  int32_t out, rop;
+  int32_t term_begin, term_end;  // into the key's Term list
+};
+struct Term {
+  int32_t lop;
+  double coef;
+};
+
 struct Chunk {
   GemmBatch host1, host2;  // released after upload
   DeviceBatch p1, p2;
+  std::vector<CombTask> ctasks;
+  std::vector<CombOut> couts;
+  std::vector<CombTerm> cterms;
+  CombTask* d_ctasks = nullptr;
+  CombOut* d_couts = nullptr;
+  CombTerm* d_cterms = nullptr;
+  int64_t nctasks = 0;
   int64_t ws_doubles = 0;
-  int64_t flops1 = 0, flops2 = 0;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t flops0 = 0, flops1 = 0, flops2 = 0;
+  int64_t bytes0 = 0;
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
 }  // namespace
@@ -118,6 +140,17 @@ std::vector<int32_t> shift_table(int nops, const int32_t* delta, int nsec, const
     std::copy(it->second.begin(), it->second.end(), out.begin() + (size_t)o * nsec);
   }
   return out;
+}
+
+template <class T>
+int upload_vec(const std::vector<T>& v, T** out) {
+  *out = nullptr;
+  if (v.empty()) return SDMRG_OK;
+  int rc = cuda_check(cudaMalloc(out, v.size() * sizeof(T)), "cudaMalloc combine list");
+  if (!rc)
+    rc = cuda_check(cudaMemcpy(*out, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice),
+                    "upload combine list");
+  return rc;
 }
 
 }  // namespace
@@ -212,6 +245,47 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
                      [](const Member& a, const Member& b) { return a.out < b.out; });
   }
 
+  // ---- phase-2 products: per group, members with the same right operator
+  // share T(i, b); their left operators are pre-summed (combine.cuh).  Terms
+  // of one (group, rop) are ordered by left op; duplicate left ops sum their
+  // scales in member (table-row) order.
+  std::vector<std::vector<Pair>> pairs(nk);
+  std::vector<std::vector<Term>> terms(nk);
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t i = 0; i < nk; ++i) {
+    const auto& mem = per_key[i];
+    std::vector<Pair>& pv = pairs[i];
+    std::vector<Term>& tv = terms[i];
+    std::vector<int64_t> idx;
+    for (size_t a = 0; a < mem.size();) {
+      size_t b = a;
+      while (b < mem.size() && mem[b].out == mem[a].out) ++b;
+      idx.resize(b - a);
+      std::iota(idx.begin(), idx.end(), (int64_t)a);
+      std::stable_sort(idx.begin(), idx.end(), [&](int64_t x, int64_t y) {
+        const int32_t rx = d->rop[mem[x].row], ry = d->rop[mem[y].row];
+        if (rx != ry) return rx < ry;
+        return d->lop[mem[x].row] < d->lop[mem[y].row];
+      });
+      for (size_t u = 0; u < idx.size();) {
+        const int32_t ro = d->rop[mem[idx[u]].row];
+        Pair p{mem[a].out, ro, static_cast<int32_t>(tv.size()), 0};
+        size_t v = u;
+        while (v < idx.size() && d->rop[mem[idx[v]].row] == ro) {
+          const int32_t lo = d->lop[mem[idx[v]].row];
+          double coef = 0.0;
+          while (v < idx.size() && d->rop[mem[idx[v]].row] == ro && d->lop[mem[idx[v]].row] == lo)
+            coef += mem[idx[v++]].scale;
+          if (coef != 0.0) tv.push_back({lo, coef});
+        }
+        p.term_end = static_cast<int32_t>(tv.size());
+        if (p.term_end > p.term_begin) pv.push_back(p);
+        u = v;
+      }
+      a = b;
+    }
+  }
+
   // ---- statistics in the reference's FLOP convention (sbmm4s.py:205)
   int64_t groups = 0, members = 0, ref_flops = 0;
   std::vector<double> key_cost(nk, 0.0);
@@ -225,10 +299,12 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       const int64_t p = (int64_t)(b - a);
       const int64_t q = d->dim_l[keys[mem[a].out].jl], r = d->dim_r[keys[mem[a].out].jr];
       ref_flops += 2 * m * r * n * p + 2 * q * r * m * p;
-      key_cost[i] += double(2 * q * r * m * p);
       ++groups;
       a = b;
     }
+    // sharding cost: the executed phase-2 products of this key
+    for (const Pair& p : pairs[i])
+      key_cost[i] += 2.0 * d->dim_l[keys[p.out].jl] * d->dim_r[keys[p.out].jr] * m;
   }
   if (d->keep_groups) {
     plan->g_begin.push_back(0);
@@ -266,14 +342,17 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     }
   }
 
-  // ---- execution schedule: chunks of ψ keys bounded by T workspace
-  std::vector<int64_t> t_need(nk, 0);  // doubles of distinct non-identity T per key
-  std::vector<std::vector<std::pair<int32_t, int64_t>>> t_slots(nk);  // (rop, ws offset|-1)
+  // ---- execution schedule: chunks of ψ keys bounded by the workspace
+  // (distinct non-identity T blocks + pre-summed left operators per key)
+  std::vector<int64_t> t_need(nk, 0);
   for (int64_t i = 0; i < nk; ++i) {
     if (!mine[i]) continue;
     const int64_t m = d->dim_l[keys[i].jl];
     std::vector<int32_t> rops;
-    for (const Member& mb : per_key[i]) rops.push_back(d->rop[mb.row]);
+    for (const Pair& p : pairs[i]) {
+      rops.push_back(p.rop);
+      if (p.term_end - p.term_begin > 1) t_need[i] += (int64_t)d->dim_l[keys[p.out].jl] * m;
+    }
     std::sort(rops.begin(), rops.end());
     rops.erase(std::unique(rops.begin(), rops.end()), rops.end());
     for (int32_t ro : rops) {
@@ -296,12 +375,14 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   budget = std::min(budget, std::max<int64_t>(total_t, 1));
 
   int64_t exec_flops = 0, local_members = 0, t_problems = 0, tiles = 0, segments = 0;
+  int64_t products = 0, comb_outputs = 0, comb_terms = 0;
   double algo_bytes = 16.0 * off;
   {
     // unique operator blocks touched (compulsory reads)
     std::vector<char> seen_l((size_t)d->nops_l * nL, 0), seen_r((size_t)d->nops_r * nR, 0);
     for (int64_t i = 0; i < nk; ++i) {
       if (!mine[i]) continue;
+      local_members += (int64_t)per_key[i].size();
       for (const Member& mb : per_key[i]) {
         const int lo = d->lop[mb.row], ro = d->rop[mb.row];
         char& sl = seen_l[(size_t)lo * nL + keys[i].jl];
@@ -333,9 +414,9 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       if (!mine[i]) continue;
       const Key& k = keys[i];
       const int m = d->dim_l[k.jl], n = d->dim_r[k.jr];
-      for (const Member& mb : per_key[i]) {
-        const int ro = d->rop[mb.row];
-        auto& tm = tmap[i - i0];
+      auto& tm = tmap[i - i0];
+      for (const Pair& pr : pairs[i]) {
+        const int ro = pr.rop;
         if (tm.count(ro)) continue;
         if (d->kind_r[ro] == 1) {  // R = identity: T = A (no product)
           tm[ro] = {make_handle(B_PSI, plan->offs[i]), n};
@@ -354,27 +435,54 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
         ++t_problems;
       }
     }
-    // phase 2: one problem per out key, segments ordered (ψ key, row)
-    std::map<int32_t, std::vector<std::pair<int64_t, const Member*>>> by_out;
+    // phase 0 + 2: one σ problem per out key; one segment per (ψ key, right
+    // op) product, ordered (ψ key, rop); multi-term left sums staged by the
+    // combine kernel into the workspace after the T blocks
+    std::map<int32_t, std::vector<std::pair<int64_t, const Pair*>>> by_out;
     for (int64_t i = i0; i < i1; ++i) {
       if (!mine[i]) continue;
-      for (const Member& mb : per_key[i]) by_out[mb.out].push_back({i, &mb});
+      for (const Pair& pr : pairs[i]) by_out[pr.out].push_back({i, &pr});
     }
     for (auto& kv : by_out) {
       const int32_t o = kv.first;
       const int q = d->dim_l[keys[o].jl], r = d->dim_r[keys[o].jr];
       ch.host2.begin_prob(make_handle(B_SIGMA, plan->offs[o]), r, q, r, 1);
-      for (auto& e : kv.second) {
-        const int64_t i = e.first;
-        const Member& mb = *e.second;
+      for (size_t u = 0; u < kv.second.size();) {
+        const int64_t i = kv.second[u].first;
         const int m = d->dim_l[keys[i].jl];
-        const int lo = d->lop[mb.row], ro = d->rop[mb.row];
-        const auto& th = tmap[i - i0].at(ro);
-        ch.host2.add_seg(make_handle(B_ARENA_L, d->blk_off_l[(int64_t)lo * nL + keys[i].jl]), m,
-                         th.first, th.second, m, mb.scale);
-        exec_flops += 2LL * q * r * m;
-        ch.flops2 += 2LL * q * r * m;
-        ++local_members;
+        const int qm = q * m;
+        const int32_t out_first = static_cast<int32_t>(ch.couts.size());
+        for (; u < kv.second.size() && kv.second[u].first == i; ++u) {
+          const Pair& pr = *kv.second[u].second;
+          const Term* tt = terms[i].data();
+          const auto& th = tmap[i - i0].at(pr.rop);
+          if (pr.term_end - pr.term_begin == 1) {
+            const Term& t = tt[pr.term_begin];
+            ch.host2.add_seg(make_handle(B_ARENA_L, d->blk_off_l[(int64_t)t.lop * nL + keys[i].jl]),
+                             m, th.first, th.second, m, t.coef);
+          } else {
+            CombOut co{make_handle(B_WS, ws), static_cast<int32_t>(ch.cterms.size()), 0};
+            for (int32_t x = pr.term_begin; x < pr.term_end; ++x)
+              ch.cterms.push_back(
+                  {make_handle(B_ARENA_L, d->blk_off_l[(int64_t)tt[x].lop * nL + keys[i].jl]),
+                   tt[x].coef});
+            co.term_end = static_cast<int32_t>(ch.cterms.size());
+            ch.couts.push_back(co);
+            ch.host2.add_seg(make_handle(B_WS, ws), m, th.first, th.second, m, 1.0);
+            ws += qm;
+            ch.flops0 += 2LL * (co.term_end - co.term_begin) * qm;
+            ch.bytes0 += 8LL * (co.term_end - co.term_begin + 1) * qm;
+            ++comb_outputs;
+            comb_terms += co.term_end - co.term_begin;
+          }
+          exec_flops += 2LL * q * r * m;
+          ch.flops2 += 2LL * q * r * m;
+          ++products;
+        }
+        const int32_t out_last = static_cast<int32_t>(ch.couts.size());
+        if (out_last > out_first)
+          for (int e0 = 0; e0 < qm; e0 += COMB_CHUNK)
+            ch.ctasks.push_back({out_first, out_last, e0, std::min(COMB_CHUNK, qm - e0)});
       }
       ch.host2.end_prob();
     }
@@ -398,8 +506,15 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     if (rc) break;
     rc = ch.host1.upload(&ch.p1, 0);
     if (!rc) rc = ch.host2.upload(&ch.p2, 0);
+    if (!rc) rc = upload_vec(ch.ctasks, &ch.d_ctasks);
+    if (!rc) rc = upload_vec(ch.couts, &ch.d_couts);
+    if (!rc) rc = upload_vec(ch.cterms, &ch.d_cterms);
+    ch.nctasks = static_cast<int64_t>(ch.ctasks.size());
     ch.host1 = GemmBatch();
     ch.host2 = GemmBatch();
+    ch.ctasks = std::vector<CombTask>();
+    ch.couts = std::vector<CombOut>();
+    ch.cterms = std::vector<CombTerm>();
   }
   if (rc) {
     sdmrg_plan_destroy(plan);
@@ -419,9 +534,13 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   st.chunks = static_cast<int64_t>(plan->chunks.size());
   st.workspace_doubles = ws_max;
   int64_t kernels = 0;
-  for (auto& ch : plan->chunks) kernels += (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0);
+  for (auto& ch : plan->chunks)
+    kernels += (ch.nctasks > 0) + (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0);
   st.kernels_per_apply = kernels;
   st.algo_bytes = static_cast<int64_t>(algo_bytes);
+  st.products = products;
+  st.combine_outputs = comb_outputs;
+  st.combine_terms = comb_terms;
   *out = plan;
   return SDMRG_OK;
 }
@@ -474,15 +593,26 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
   for (size_t c = 0; c < plan->chunks.size(); ++c) {
     Chunk& ch = plan->chunks[c];
     if (plan->timing) cudaEventRecord(ch.ev[0], stream);
-    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 2 * c, stream);
-    if (rc) return rc;
+    if (ch.nctasks > 0) {
+      combine_kernel<<<static_cast<unsigned>(ch.nctasks), COMB_THREADS, 0, stream>>>(
+          ch.d_ctasks, ch.d_couts, ch.d_cterms, bases);
+      count_launch();
+      rc = cuda_check(cudaGetLastError(), "combine_kernel launch");
+      if (rc) return rc;
+    }
     if (plan->timing) {
       cudaEventRecord(ch.ev[1], stream);
       cudaEventRecord(ch.ev[2], stream);
     }
+    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 2 * c, stream);
+    if (rc) return rc;
+    if (plan->timing) {
+      cudaEventRecord(ch.ev[3], stream);
+      cudaEventRecord(ch.ev[4], stream);
+    }
     rc = launch_engine(false, false, ch.p2, bases, plan->counters + 2 * c + 1, stream);
     if (rc) return rc;
-    if (plan->timing) cudaEventRecord(ch.ev[3], stream);
+    if (plan->timing) cudaEventRecord(ch.ev[5], stream);
   }
   return SDMRG_OK;
 }
@@ -500,25 +630,32 @@ int sdmrg_plan_set_timing(sdmrg_plan* plan, int enable) {
   return SDMRG_OK;
 }
 
-int sdmrg_plan_timing(sdmrg_plan* plan, double* ms1, double* ms2, int64_t* f1, int64_t* f2) {
+int sdmrg_plan_timing(sdmrg_plan* plan, double* ms, int64_t* flops, int64_t* bytes) {
   if (!plan || !plan->timing) return fail(SDMRG_EINVAL, "plan_timing: timing not enabled");
-  double t1 = 0.0, t2 = 0.0;
-  int64_t a = 0, b = 0;
+  double t[3] = {0.0, 0.0, 0.0};
+  int64_t f[3] = {0, 0, 0};
+  int64_t by = 0;
   for (auto& ch : plan->chunks) {
-    int rc = cuda_check(cudaEventSynchronize(ch.ev[3]), "timing sync");
+    int rc = cuda_check(cudaEventSynchronize(ch.ev[5]), "timing sync");
     if (rc) return rc;
-    float x = 0.f, y = 0.f;
-    cudaEventElapsedTime(&x, ch.ev[0], ch.ev[1]);
-    cudaEventElapsedTime(&y, ch.ev[2], ch.ev[3]);
-    t1 += x;
-    t2 += y;
-    a += ch.flops1;
-    b += ch.flops2;
+    for (int p = 0; p < 3; ++p) {
+      float x = 0.f;
+      cudaEventElapsedTime(&x, ch.ev[2 * p], ch.ev[2 * p + 1]);
+      t[p] += x;
+    }
+    f[0] += ch.flops0;
+    f[1] += ch.flops1;
+    f[2] += ch.flops2;
+    by += ch.bytes0;
   }
-  if (ms1) *ms1 = t1;
-  if (ms2) *ms2 = t2;
-  if (f1) *f1 = a;
-  if (f2) *f2 = b;
+  for (int p = 0; p < 3; ++p) {
+    if (ms) ms[p] = t[p];
+    if (flops) flops[p] = f[p];
+  }
+  if (bytes) {
+    bytes[0] = by;
+    bytes[1] = bytes[2] = 0;
+  }
   return SDMRG_OK;
 }
 
@@ -527,6 +664,9 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
   for (auto& ch : plan->chunks) {
     ch.p1.release();
     ch.p2.release();
+    if (ch.d_ctasks) cudaFree(ch.d_ctasks);
+    if (ch.d_couts) cudaFree(ch.d_couts);
+    if (ch.d_cterms) cudaFree(ch.d_cterms);
     for (auto& e : ch.ev)
       if (e) cudaEventDestroy(e);
   }

@@ -177,12 +177,13 @@ class DevicePlan:
         _lib.check(_lib.load().sdmrg_plan_set_timing(self._h, int(bool(enable))))
 
     def last_timing(self):
-        """(ms phase 1, ms phase 2, flops phase 1, flops phase 2) of the last apply."""
-        m1, m2 = ctypes.c_double(), ctypes.c_double()
-        f1, f2 = ctypes.c_int64(), ctypes.c_int64()
-        _lib.check(_lib.load().sdmrg_plan_timing(self._h, ctypes.byref(m1), ctypes.byref(m2),
-                                                 ctypes.byref(f1), ctypes.byref(f2)))
-        return m1.value, m2.value, f1.value, f2.value
+        """Per-phase device ms, executed FLOPs and algorithmic bytes of the last
+        apply: phase 0 left-operator pre-summation, 1 T = A R^T, 2 σ += Lsum T."""
+        ms = (ctypes.c_double * 3)()
+        fl = (ctypes.c_int64 * 3)()
+        by = (ctypes.c_int64 * 3)()
+        _lib.check(_lib.load().sdmrg_plan_timing(self._h, ms, fl, by))
+        return list(ms), list(fl), list(by)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -1,5 +1,5 @@
 """Quick per-phase timing of one H_eff·ψ workload (experiments)."""
-import json, os, subprocess, sys
+import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
@@ -15,12 +15,15 @@ out = plan.empty_vector()
 for _ in range(2):
     plan.apply(psi, out)
 plan.set_timing(True)
-res = []
+res = [None] * 3
 for _ in range(3):
     plan.apply(psi, out)
-    res.append(plan.last_timing())
-m1 = min(r[0] for r in res); m2 = min(r[1] for r in res)
-f1, f2 = res[0][2], res[0][3]
+    res[_] = plan.last_timing()
+ms = [min(r[0][k] for r in res) for k in range(3)]
+fl, by = res[0][1], res[0][2]
 print(json.dumps({"lib": os.environ.get("SDMRG_LIB", "default"), "L": L, "D": D,
-                  "ms": [round(m1, 2), round(m2, 2)], "tflops": [round(f1 / m1 / 1e9, 2), round(f2 / m2 / 1e9, 2)],
-                  "total_ms": round(m1 + m2, 2), "ref_tflops": round(plan.stats["ref_flops"] / (m1 + m2) / 1e9, 2)}))
+                  "ms": [round(x, 2) for x in ms],
+                  "tflops": [round(f / max(m, 1e-9) / 1e9, 2) for f, m in zip(fl, ms)],
+                  "combine_GBs": round(by[0] / max(ms[0], 1e-9) / 1e6, 1),
+                  "total_ms": round(sum(ms), 2),
+                  "ref_tflops": round(plan.stats["ref_flops"] / sum(ms) / 1e9, 2)}))
