@@ -284,7 +284,7 @@ def run_b200(args):
         step(psi, sigma)
         ph.append(plan.last_timing())
     plan.set_timing(False)
-    phase_ms = [float(np.mean([p[0][k] for p in ph])) for k in range(3)]
+    phase_ms = [float(np.mean([p[0][k] for p in ph])) for k in range(4)]
     phase_flops, phase_bytes = ph[0][1], ph[0][2]
 
     # e2e: host ψ in (pinned), σ back every step, through the public API
@@ -340,9 +340,10 @@ def run_b200(args):
     value = st["ref_flops"] / (ms * 1e-3) / 1e12
     dom = int(np.argmax(phase_ms))
     names = ["combine_kernel (phase 0: Lsum = sum s L)", "seg_gemm_kernel<0,1> (phase 1: T = A R^T)",
-             "seg_gemm_kernel<0,0> (phase 2: sigma += Lsum T)"]
-    if dom == 0:
-        achieved = phase_bytes[0] / (phase_ms[0] * 1e-3) / 1e9
+             "seg_gemm_kernel<0,0> (phase 2: sigma += Lsum T)",
+             "combine_kernel (phase 3: split-K partials into sigma)"]
+    if dom in (0, 3):
+        achieved = phase_bytes[dom] / (phase_ms[dom] * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak(), "unit": "GB/s"}
     else:
         achieved = phase_flops[dom] / (phase_ms[dom] * 1e-3) / 1e12
@@ -350,9 +351,9 @@ def run_b200(args):
     roof.update({"frac": roof["achieved"] / roof["peak"] if roof["peak"] else None,
                  "traffic": None, "kernel": names[dom],
                  "peak_source": ("measured live: cuBLAS DGEMM 8192^3 burst (torch.matmul f64)"
-                                 if dom else "MEASURED_PEAKS.json hbm_gbs"),
+                                 if dom in (1, 2) else "MEASURED_PEAKS.json hbm_gbs"),
                  "phase_ms": phase_ms, "phase_exec_flops": phase_flops,
-                 "phase0_bytes": phase_bytes[0]})
+                 "phase_bytes": phase_bytes})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

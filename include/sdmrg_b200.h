@@ -186,9 +186,10 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma,
                      int accumulate, void* stream);
 /* Per-launch CUDA-event timing of subsequent applies (bench instrumentation).
  * sdmrg_plan_timing syncs the last apply's events and writes, per phase
- * (0: left-operator pre-summation, 1: T = A R^T, 2: σ += Lsum T), the summed
- * device milliseconds ms[3], the executed FLOPs flops[3] and (phase 0 only)
- * the algorithmic bytes bytes[3].  Any pointer may be NULL.                 */
+ * (0: left-operator pre-summation, 1: T = A R^T, 2: σ += Lsum T, 3: split-K
+ * partial sums into σ), the summed device milliseconds ms[4], the executed
+ * tensor FLOPs flops[4] and the algorithmic bytes of the elementwise phases
+ * bytes[4].  Any pointer may be NULL.                                        */
 int sdmrg_plan_set_timing(sdmrg_plan* plan, int enable);
 int sdmrg_plan_timing(sdmrg_plan* plan, double* ms, int64_t* flops, int64_t* bytes);
 int sdmrg_plan_destroy(sdmrg_plan* plan);

@@ -1,4 +1,5 @@
-// engine.cuh — persistent segmented grouped GEMM in FP64 for sm_100a.
+// engine.cuh — persistent, warp-specialized segmented grouped GEMM in FP64
+// for sm_100a.
 //
 // One kernel family executes every dense contraction of the H_eff·ψ /
 // renormalization path:
@@ -6,25 +7,38 @@
 //     C_p  =  beta_p * C_p  +  sum_{s in segs(p)}  scale_s * opA_s @ opB_s
 //
 // over a flat list of output tiles (<= 64 x 64) drawn from many problems p of
-// arbitrary size.  The K dimension of a problem is a *list of segments*: this
-// is SBMM4S's concatenated GEMM (sbmm4s.py:150 concat_gemm_accumulate — the
+// arbitrary size.  The K dimension of a problem is a *list of segments*:
+// SBMM4S's concatenated GEMM (sbmm4s.py:155 concat_gemm_accumulate — the
 // horizontally concatenated L stack times the vertically concatenated temp)
-// without requiring the members to be contiguous, so the "sum over members"
-// is carried by the shared inner dimension and no reduction pass exists
-// (sbmm4s.py:1-12, paper §II.C).  Each tile is owned by exactly one CTA, so
-// accumulation order is fixed and results are deterministic.
+// without requiring the members to be contiguous, so the sum over members is
+// carried by the shared inner dimension and no reduction pass exists
+// (sbmm4s.py:1-12, paper §II.C).  Each tile has exactly one owner CTA, so
+// the accumulation order is fixed and results are bitwise deterministic.
 //
 // Math: DMMA (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4).  tcgen05 has no f64
-// kind; on B200 the FP64 tensor pipe is reached through DMMA (measured 37.1
-// TFLOP/s issue ceiling, profiles/).  Staging: 3-stage cp.async (LDGSTS.64)
-// ring in shared memory; sector blocks have odd leading dimensions, hence
-// 8-byte async copies.
+// kind; on B200 the FP64 pipe is shared by DMMA and DFMA (37.1 / 36.7
+// TFLOP/s measured, tools/fp64_probe.cu) and cuBLAS's own DGEMM is a DMMA
+// kernel (cutlass_80_tensorop_d884gemm, profiles/r1a_launches.txt).
 //
-// Shape handling: the host cuts every problem into *balanced* tiles (a
-// 138-row sector becomes 48+48+42, not 64+64+10) and each CTA splits its
-// tile's 8x8 blocks evenly over a 2x2 warp grid, so the four warps issue the
-// same number of DMMAs per stage.  A warp's (rows, cols) block count selects a
-// branch-free DMMA body (no predicated mma.sync).
+// CTA = 1 producer warp + 4 consumer warps, 3 CTAs per SM (persistent):
+//   producer  pulls tiles from a global counter (one tile of lookahead, the
+//             next tile's descriptor and first segment prefetched), walks
+//             their segments and streams 16-deep K stages of both operands
+//             into a STAGES-deep shared-memory ring with 8-byte cp.async
+//             (sector blocks have odd leading dimensions: neither TMA nor
+//             16-byte copies apply).  Completion is signalled through
+//             mbarriers (cp.async.mbarrier.arrive.noinc), so descriptor and
+//             global-memory latency never stalls the math warps and the ring
+//             runs continuously across tile boundaries;
+//   consumers a 2 x 2 warp grid over the tile's 8x8 blocks, balanced (a warp
+//             owns up to 4 x 4 blocks, 32 accumulators).  The (row blocks,
+//             col blocks) shape is dispatched once per tile into a
+//             branch-free DMMA body that loops over the tile's stages and
+//             ends in the epilogue (stores straight from registers).
+// Why 64 x 64 and 4 math warps per tile: the sector problems are small
+// (L=30, D=2048: flop-weighted 124 x 119 x 129 in phase 1, output sectors
+// <= 183 in phase 2); a 128 x 128 CTA tile with 8 warps left each warp 8
+// DMMAs per k4 step on typical tiles and ran at 12-16 TFLOP/s (profiles/n4a).
 //
 // Shared-memory layouts per stage (doubles):
 //   K-contiguous operand tile [64][16], XOR-swizzled on 4-wide k groups:
@@ -50,6 +64,10 @@ struct Bases {
   double* p[kMaxBases];
 };
 
+__device__ __forceinline__ const double* resolve(const Bases& bases, uint64_t h) {
+  return bases.p[h >> kHandleShift] + (h & kHandleMask);
+}
+
 struct Prob {        // 32 B
   uint64_t c;        // handle of C(0,0); C row-major, ldc
   int32_t ldc;
@@ -60,7 +78,17 @@ struct Prob {        // 32 B
 struct Tile {        // 16 B
   int32_t prob;
   int32_t row0, col0;
-  int16_t tm, tn;    // tile extents (<= 64)
+  int16_t tm, tn;    // tile extents (<= 128)
+};
+// Device form of a tile: the problem fields folded in, so the producer needs
+// one dependent load (tile -> segment) instead of two.
+struct TileRec {     // 40 B
+  uint64_t c;        // handle of C(0,0) of the problem
+  int32_t ldc, beta;
+  int32_t seg_begin, seg_end;
+  int32_t row0, col0;
+  int16_t tm, tn;
+  int32_t pad;
 };
 struct Seg {         // 40 B
   uint64_t a;        // handle of opA(0,0)
@@ -72,38 +100,72 @@ struct Seg {         // 40 B
 };
 
 #ifndef SDMRG_STAGES
-#define SDMRG_STAGES 3
+#define SDMRG_STAGES 4
 #endif
 #ifndef SDMRG_MINB
 #define SDMRG_MINB 3
 #endif
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = SDMRG_STAGES, THREADS = 128;
-constexpr int PADN = 4;                        // padding of M/N-contiguous tiles
-constexpr int KC_ELEMS = 64 * BK;              // K-contiguous tile
-constexpr int NC_ELEMS = BK * (64 + PADN);     // M/N-contiguous tile
+constexpr int BM = 64, BN = 64, BK = 16, STAGES = SDMRG_STAGES;
+constexpr int CONSUMERS = 4, WGRID_R = 2, WGRID_C = 2;
+constexpr int THREADS = 32 * (CONSUMERS + 1);
+constexpr int PADN = 4;                          // padding of M/N-contiguous tiles
+constexpr int KC_ELEMS = BM * BK;                // K-contiguous tile (BM == BN)
+constexpr int NC_LD = BM + PADN;
+constexpr int NC_ELEMS = BK * NC_LD;             // M/N-contiguous tile
 template <bool TA>
 __host__ __device__ constexpr int a_elems() { return TA ? NC_ELEMS : KC_ELEMS; }
 template <bool TB>
 __host__ __device__ constexpr int b_elems() { return TB ? KC_ELEMS : NC_ELEMS; }
 template <bool TA, bool TB>
 __host__ __device__ constexpr int stage_elems() { return a_elems<TA>() + b_elems<TB>(); }
-template <bool TA, bool TB>
-__host__ __device__ constexpr int smem_bytes() { return STAGES * stage_elems<TA, TB>() * 8; }
 
-__device__ __forceinline__ const double* resolve(const Bases& bases, uint64_t h) {
-  return bases.p[h >> kHandleShift] + (h & kHandleMask);
+// Per-stage metadata written by the producer's lane 0.
+struct StageMeta {
+  double* c;         // tile origin in C (first stage of a tile)
+  double scale;
+  int32_t nks;       // k4 steps in this stage (0: no K, or kEnd)
+  int32_t flags;
+  int32_t ldc, beta;
+  int16_t tm, tn;
+  int32_t pad;
+};
+constexpr int kFirst = 1, kLast = 2, kEnd = 4;
+
+template <bool TA, bool TB>
+__host__ __device__ constexpr int smem_bytes() {
+  return STAGES * stage_elems<TA, TB>() * 8 + STAGES * (int)sizeof(StageMeta) + 2 * STAGES * 8 +
+         kMaxBases * 8;
 }
 
 __device__ __forceinline__ void cp_async8(uint32_t saddr, const double* gmem, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem),
                "r"(valid ? 8 : 0));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void cp_async8_full(uint32_t saddr, const double* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
 
-// Volatile on purpose: letting ptxas reorder fragment loads and DMMAs freely
-// measured 7% slower (more live registers, profiles/r1_notes.md).
+// Volatile on purpose: the issue order written here is the schedule.
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d[0]), "+d"(d[1]) : "d"(a), "d"(b));
@@ -119,282 +181,320 @@ __host__ __device__ constexpr int kc_pos(int r, int k) {
   return r * BK + ((((k >> 2) ^ (r & 3)) << 2) | (k & 3));
 }
 
-// Per-thread load geometry.  TA: opA stored M-contiguous (A(i,k) =
-// a[k*lda + i]); else K-contiguous (A(i,k) = a[i*lda + k]).  TB: opB stored
-// K-contiguous (B(k,j) = b[j*ldb + k]); else N-contiguous (b[k*ldb + j]).
-//   K-contig operand : kk = tid % 16, rows tid/16 + 8i      (i < 8)
-//   M/N-contig       : row = tid % 64, kk = tid/64 + 2i     (i < 8)
-struct SegState {
-  const double* a;   // this thread's A element 0 at the current k offset
-  const double* b;
-  int32_t a_k16, b_k16;      // element step of the bases per stage (+16 in k)
-  int32_t a_istep, b_istep;  // element step between the thread's 8 elements
-  int32_t kleft;             // k remaining in this segment from the offset
-  double scale;
+// Shared state of one CTA's pipeline.
+struct Ring {
+  uint32_t smem;     // shared address of stage 0
+  uint32_t full0;    // full barriers (STAGES x 8 bytes), then empty barriers
+  uint32_t empty0;
+  StageMeta* meta;
 };
 
-template <bool TA, bool TB>
-__device__ __forceinline__ void setup_seg(SegState& st, const Seg& s, const Bases& bases,
-                                          int row0, int col0, int tid) {
-  const double* a = resolve(bases, s.a);
-  const double* b = resolve(bases, s.b);
-  if (!TA) {
-    st.a = a + (int64_t)(row0 + tid / BK) * s.lda + (tid % BK);
-    st.a_k16 = BK;
-    st.a_istep = 8 * s.lda;
-  } else {
-    st.a = a + (int64_t)(tid / 64) * s.lda + row0 + (tid % 64);
-    st.a_k16 = BK * s.lda;
-    st.a_istep = 2 * s.lda;
-  }
-  if (TB) {
-    st.b = b + (int64_t)(col0 + tid / BK) * s.ldb + (tid % BK);
-    st.b_k16 = BK;
-    st.b_istep = 8 * s.ldb;
-  } else {
-    st.b = b + (int64_t)(tid / 64) * s.ldb + col0 + (tid % 64);
-    st.b_k16 = BK * s.ldb;
-    st.b_istep = 2 * s.ldb;
-  }
-  st.kleft = s.k;
-  st.scale = s.scale;
-}
-
-__device__ __forceinline__ void cp_async8_full(uint32_t saddr, const double* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem));
-}
-
-// Branch-free DMMA body over one stage for a warp owning MB x NB 8x8 blocks.
-// a_ks[ks] / b_ks[ks]: per-thread byte address of fragment (block 0, k4 ks).
+// ------------------------------------------------------------------ consumer
+// A warp owning MB x NB 8x8 blocks of a tile: runs every stage of the tile
+// (the first one already waited for), then the epilogue.  a_off/b_off: byte
+// offset of fragment (block 0, k4 step 0) within a stage; g = row & 3 of the
+// fragment rows (K-contiguous swizzle group).
 template <bool TA, bool TB, int MB, int NB>
-__device__ __forceinline__ void mma_stage(double (&acc)[4][4][2], const uint32_t (&a_ks)[4],
-                                          const uint32_t (&b_ks)[4], int nks, double scale) {
-  constexpr int A_I = TA ? 8 * 8 : 8 * BK * 8;           // next 8-row block (bytes)
-  constexpr int B_J = TB ? 8 * BK * 8 : 8 * 8;           // next 8-col block
-  const bool scaled = scale != 1.0;
+__device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint32_t& phase,
+                                             uint32_t a_off, uint32_t b_off, int g, double* c,
+                                             int ldc, int beta, int row_lim, int col_lim,
+                                             int lane) {
+  constexpr uint32_t STAGE_B = stage_elems<TA, TB>() * 8;
+  constexpr int A_I = TA ? 8 * 8 : 8 * BK * 8;            // next 8-row block (bytes)
+  constexpr int B_J = TB ? 8 * BK * 8 : 8 * 8;            // next 8-col block
+  constexpr int NC_KS = 4 * NC_LD * 8;                    // next k4 step, M/N-contiguous
+  double acc[MB > 0 ? MB : 1][NB > 0 ? NB : 1][2];
 #pragma unroll
-  for (int ks = 0; ks < BK / 4; ++ks) {
-    if (ks < nks) {
-      double af[MB], bf[NB];
+  for (int i = 0; i < MB; ++i)
 #pragma unroll
-      for (int i = 0; i < MB; ++i) af[i] = lds64(a_ks[ks] + i * A_I);
+    for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // K-contiguous (swizzled) tiles: step ks of a fragment whose row has
+  // (row & 3) == g sits at 32-byte group (ks ^ g); the offsets already point
+  // at group g.
+  int ksw[4];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) bf[j] = lds64(b_ks[ks] + j * B_J);
-      if (scaled) {
+  for (int ks = 0; ks < 4; ++ks) ksw[ks] = ((ks ^ g) - g) << 5;
+  while (true) {
+    const StageMeta& m = ring.meta[stage];
+    const int flags = m.flags;
+    const int nks = m.nks;
+    const double scale = m.scale;
+    const uint32_t a0 = ring.smem + stage * STAGE_B + a_off;
+    const uint32_t b0 = ring.smem + stage * STAGE_B + b_off;
+    if (MB > 0 && NB > 0) {
+      const bool scaled = scale != 1.0;
 #pragma unroll
-        for (int i = 0; i < MB; ++i) af[i] *= scale;
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        if (ks < nks) {
+          double af[MB > 0 ? MB : 1], bf[NB > 0 ? NB : 1];
+#pragma unroll
+          for (int i = 0; i < MB; ++i)
+            af[i] = lds64(TA ? a0 + ks * NC_KS + i * A_I : a0 + i * A_I + ksw[ks]);
+#pragma unroll
+          for (int j = 0; j < NB; ++j)
+            bf[j] = lds64(TB ? b0 + j * B_J + ksw[ks] : b0 + ks * NC_KS + j * B_J);
+          if (scaled) {
+            if (NB <= MB) {
+#pragma unroll
+              for (int j = 0; j < NB; ++j) bf[j] *= scale;
+            } else {
+#pragma unroll
+              for (int i = 0; i < MB; ++i) af[i] *= scale;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < MB; ++i)
+#pragma unroll
+            for (int j = 0; j < NB; ++j) dmma(acc[i][j], af[i], bf[j]);
+        }
       }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(ring.empty0 + 8 * stage);
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+    if (flags & kLast) break;
+    mbar_wait(ring.full0 + 8 * stage, phase);
+  }
+  // epilogue: masked store (optionally accumulating); row_lim/col_lim are the
+  // tile extents relative to this thread's first row / column
 #pragma unroll
-      for (int i = 0; i < MB; ++i)
+  for (int i = 0; i < MB; ++i) {
+    if (8 * i < row_lim) {
+      double* crow = c + (int64_t)(8 * i) * ldc;
 #pragma unroll
-        for (int j = 0; j < NB; ++j) dmma(acc[i][j], af[i], bf[j]);
+      for (int j = 0; j < NB; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (8 * j + h < col_lim) {
+            double v = acc[i][j][h];
+            if (beta) v += crow[8 * j + h];
+            crow[8 * j + h] = v;
+          }
+        }
+      }
     }
   }
 }
 
-template <bool TA, bool TB, int MB>
-__device__ __forceinline__ void mma_stage_nb(double (&acc)[4][4][2], const uint32_t (&a)[4],
-                                             const uint32_t (&b)[4], int nblk, int nks,
-                                             double scale) {
-  switch (nblk) {
-    case 4: mma_stage<TA, TB, MB, 4>(acc, a, b, nks, scale); break;
-    case 3: mma_stage<TA, TB, MB, 3>(acc, a, b, nks, scale); break;
-    case 2: mma_stage<TA, TB, MB, 2>(acc, a, b, nks, scale); break;
-    case 1: mma_stage<TA, TB, MB, 1>(acc, a, b, nks, scale); break;
-    default: break;
+#define SDMRG_TILE_CASE(MB, NB)                                                              \
+  case (MB) * 8 + (NB):                                                                      \
+    consume_tile<TA, TB, MB, NB>(ring, stage, phase, a_off, b_off, g, c, ldc, beta, row_lim, \
+                                 col_lim, lane);                                             \
+    break;
+
+template <bool TA, bool TB>
+__device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring& ring, int& stage,
+                                                 uint32_t& phase, uint32_t a_off, uint32_t b_off,
+                                                 int g, double* c, int ldc, int beta, int row_lim,
+                                                 int col_lim, int lane) {
+  switch (mblk * 8 + nblk) {
+    SDMRG_TILE_CASE(4, 4) SDMRG_TILE_CASE(4, 3) SDMRG_TILE_CASE(4, 2) SDMRG_TILE_CASE(4, 1)
+    SDMRG_TILE_CASE(3, 4) SDMRG_TILE_CASE(3, 3) SDMRG_TILE_CASE(3, 2) SDMRG_TILE_CASE(3, 1)
+    SDMRG_TILE_CASE(2, 4) SDMRG_TILE_CASE(2, 3) SDMRG_TILE_CASE(2, 2) SDMRG_TILE_CASE(2, 1)
+    SDMRG_TILE_CASE(1, 4) SDMRG_TILE_CASE(1, 3) SDMRG_TILE_CASE(1, 2) SDMRG_TILE_CASE(1, 1)
+    default:  // no blocks for this warp: walk the tile's stages
+      consume_tile<TA, TB, 0, 0>(ring, stage, phase, a_off, b_off, g, c, ldc, beta, row_lim,
+                                 col_lim, lane);
+      break;
+  }
+}
+#undef SDMRG_TILE_CASE
+
+// ------------------------------------------------------------------ producer
+// Per-lane load geometry of one operand within a stage (one producer warp).
+//   K-contiguous (A when !TA, B when TB): lane -> k = lane & 15, rows
+//     (lane >> 4) + 2i, i < 32; element (r, k) at src + r*ld + k.
+//   M/N-contiguous: lane -> columns lane, lane + 32; k = 0..15; element
+//     (k, c) at src + k*ld + c.
+template <bool KCONTIG>
+__device__ __forceinline__ void load_operand(uint32_t sbase, const double* src, int ld, int extent,
+                                             int krem, int lane) {
+  if (KCONTIG) {
+    const int kk = lane & 15, r0 = lane >> 4;
+    const double* p = src + (int64_t)r0 * ld + kk;
+    // rows r0 + 2i: (r & 3) alternates between r0 and r0 + 2
+    const uint32_t s_even = sbase + kc_pos(r0, kk) * 8;
+    const uint32_t s_odd = sbase + kc_pos(r0 + 2, kk) * 8 - 2 * BK * 8;
+    const int nrow = (extent - r0 + 1) >> 1;
+    if (kk < krem) {
+#pragma unroll 8
+      for (int i = 0; i < nrow; ++i)
+        cp_async8_full((i & 1 ? s_odd : s_even) + i * (2 * BK * 8), p + (int64_t)(2 * i) * ld);
+    } else {
+      // zero-fill the k tail (stale shared memory may hold non-finite data)
+#pragma unroll 8
+      for (int i = 0; i < nrow; ++i)
+        cp_async8((i & 1 ? s_odd : s_even) + i * (2 * BK * 8), src, false);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = lane + 32 * j;
+      if (c < extent) {
+        const double* p = src + c;
+        const uint32_t s0 = sbase + c * 8;
+        if (krem >= BK) {
+#pragma unroll
+          for (int k = 0; k < BK; ++k) cp_async8_full(s0 + k * (NC_LD * 8), p + (int64_t)k * ld);
+        } else {
+#pragma unroll
+          for (int k = 0; k < BK; ++k)
+            cp_async8(s0 + k * (NC_LD * 8), k < krem ? p + (int64_t)k * ld : src, k < krem);
+        }
+      }
+    }
   }
 }
 
 template <bool TA, bool TB>
-__device__ __forceinline__ void mma_dispatch(double (&acc)[4][4][2], const uint32_t (&a)[4],
-                                             const uint32_t (&b)[4], int mblk, int nblk, int nks,
-                                             double scale) {
-  if (mblk == 4 && nblk == 4) {
-    mma_stage<TA, TB, 4, 4>(acc, a, b, nks, scale);
-    return;
+__device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restrict__ tiles,
+                                        int ntiles, const Seg* __restrict__ segs,
+                                        int* __restrict__ counter, double* const* sbases,
+                                        int lane) {
+  constexpr int A_EL = a_elems<TA>();
+  constexpr uint32_t STAGE_B = stage_elems<TA, TB>() * 8;
+  auto publish = [&](int stage, int nks, double scale, int flags, const TileRec& tr,
+                     double* cptr) {
+    if (lane == 0) {
+      StageMeta& m = ring.meta[stage];
+      m.nks = nks;
+      m.scale = scale;
+      m.flags = flags;
+      if (flags & kFirst) {
+        m.c = cptr;
+        m.ldc = tr.ldc;
+        m.beta = tr.beta;
+        m.tm = tr.tm;
+        m.tn = tr.tn;
+      }
+    }
+    mbar_arrive_cp_async(ring.full0 + 8 * stage);
+    if (lane == 0) mbar_arrive(ring.full0 + 8 * stage);
+  };
+  int stage = 0;
+  uint32_t phase = 0;
+  int t = 0;
+  if (lane == 0) t = atomicAdd(counter, 1);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  TileRec cur{};
+  Seg sn{};                       // prefetched next segment descriptor
+  if (t < ntiles) {
+    cur = tiles[t];
+    if (cur.seg_begin < cur.seg_end) sn = segs[cur.seg_begin];
   }
-  switch (mblk) {
-    case 4: mma_stage_nb<TA, TB, 4>(acc, a, b, nblk, nks, scale); break;
-    case 3: mma_stage_nb<TA, TB, 3>(acc, a, b, nblk, nks, scale); break;
-    case 2: mma_stage_nb<TA, TB, 2>(acc, a, b, nblk, nks, scale); break;
-    case 1: mma_stage_nb<TA, TB, 1>(acc, a, b, nblk, nks, scale); break;
-    default: break;
+  while (t < ntiles) {
+    int next = 0;
+    if (lane == 0) next = atomicAdd(counter, 1);  // one tile of lookahead
+    next = __shfl_sync(0xffffffffu, next, 0);
+    TileRec nrec{};
+    if (next < ntiles) nrec = tiles[next];
+    double* cptr = sbases[cur.c >> kHandleShift] + (cur.c & kHandleMask) +
+                   (int64_t)cur.row0 * cur.ldc + cur.col0;
+    if (cur.seg_begin == cur.seg_end) {
+      // no K at all: C = beta * C (one empty stage carries the epilogue)
+      mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
+      publish(stage, 0, 1.0, kFirst | kLast, cur, cptr);
+      if (++stage == STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+      if (next < ntiles && nrec.seg_begin < nrec.seg_end) sn = segs[nrec.seg_begin];
+    }
+    bool first = true;
+    for (int s = cur.seg_begin; s < cur.seg_end; ++s) {
+      const Seg sg = sn;
+      if (s + 1 < cur.seg_end) sn = segs[s + 1];
+      else if (next < ntiles && nrec.seg_begin < nrec.seg_end) sn = segs[nrec.seg_begin];
+      const double* a = sbases[sg.a >> kHandleShift] + (sg.a & kHandleMask);
+      const double* b = sbases[sg.b >> kHandleShift] + (sg.b & kHandleMask);
+      // operand origins at this tile: A rows row0.., B cols col0..
+      a += TA ? cur.row0 : (int64_t)cur.row0 * sg.lda;
+      b += TB ? (int64_t)cur.col0 * sg.ldb : cur.col0;
+      for (int k0 = 0; k0 < sg.k; k0 += BK) {
+        const int krem = min(BK, sg.k - k0);
+        mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
+        const uint32_t sa = ring.smem + stage * STAGE_B;
+        const uint32_t sb = sa + A_EL * 8;
+#ifndef SDMRG_EXP_NOLOAD
+        // A: K-contig iff !TA (element (r,k) at a + r*lda + k); B: K-contig iff TB
+        load_operand<!TA>(sa, TA ? a + (int64_t)k0 * sg.lda : a + k0, sg.lda, cur.tm, krem, lane);
+        load_operand<TB>(sb, TB ? b + k0 : b + (int64_t)k0 * sg.ldb, sg.ldb, cur.tn, krem, lane);
+#endif
+        const bool last = (s + 1 == cur.seg_end) && (k0 + BK >= sg.k);
+        publish(stage, (krem + 3) >> 2, sg.scale, (first ? kFirst : 0) | (last ? kLast : 0), cur,
+                cptr);
+        first = false;
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    t = next;
+    cur = nrec;
   }
+  mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
+  publish(stage, 0, 1.0, kEnd, cur, nullptr);
 }
 
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(THREADS, SDMRG_MINB)
-seg_gemm_kernel(const Tile* __restrict__ tiles, int ntiles, const Prob* __restrict__ probs,
-                const Seg* __restrict__ segs, int* __restrict__ counter, Bases bases) {
-  extern __shared__ __align__(16) double smem[];
-  __shared__ int s_tile[2];
+seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __restrict__ segs,
+                int* __restrict__ counter, Bases bases) {
+  extern __shared__ __align__(128) double smem[];
   constexpr int A_EL = a_elems<TA>();
-  constexpr uint32_t STAGE_B = stage_elems<TA, TB>() * 8;
+  StageMeta* meta = reinterpret_cast<StageMeta*>(smem + STAGES * stage_elems<TA, TB>());
+  uint64_t* bars = reinterpret_cast<uint64_t*>(meta + STAGES);   // full[STAGES], empty[STAGES]
+  double** sbases = reinterpret_cast<double**>(bars + 2 * STAGES);
+  Ring ring;
+  ring.smem = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  ring.full0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
+  ring.empty0 = ring.full0 + STAGES * 8;
+  ring.meta = meta;
 
   const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int warp = tid >> 5;
-  const int wr = warp >> 1, wc = warp & 1;
-  const int lr = lane >> 2, lc = lane & 3;
-  const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-
-  // per-thread cp.async destinations (bytes within a stage) of element 0 and step
-  const uint32_t sa_st = TA ? ((tid / 64) * (64 + PADN) + (tid % 64)) * 8
-                            : kc_pos(tid / BK, tid % BK) * 8;
-  const uint32_t sa_step = TA ? 2 * (64 + PADN) * 8 : 8 * BK * 8;
-  const uint32_t sb_st = A_EL * 8 + (TB ? kc_pos(tid / BK, tid % BK) * 8
-                                        : ((tid / 64) * (64 + PADN) + (tid % 64)) * 8);
-  const uint32_t sb_step = TB ? 8 * BK * 8 : 2 * (64 + PADN) * 8;
-  // k index of this thread's load element 0 (+2i for M/N-contig operands)
-  const int a_k0 = TA ? tid / 64 : tid % BK;
-  const int b_k0 = TB ? tid % BK : tid / 64;
-
-  if (tid == 0) s_tile[0] = atomicAdd(counter, 1);
+  const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < kMaxBases; ++k) sbases[k] = bases.p[k];
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(ring.full0 + 8 * s, 33);          // 32 cp.async arrivals + the meta arrive
+      mbar_init(ring.empty0 + 8 * s, CONSUMERS);  // one arrive per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
-  int t = s_tile[0];
-  int flip = 0;
 
-  while (t < ntiles) {
-    if (tid == 0) s_tile[flip ^ 1] = atomicAdd(counter, 1);  // prefetch next tile index
-    const Tile tile = tiles[t];
-    const Prob prob = probs[tile.prob];
-    const int tm = tile.tm, tn = tile.tn;
-    // balanced 2x2 warp split of the tile's 8x8 blocks
+  if (warp == CONSUMERS) {
+    produce<TA, TB>(ring, tiles, ntiles, segs, counter, sbases, lane);
+    return;
+  }
+
+  // ================================================================ consumers
+  const int wr = warp / WGRID_C, wc = warp % WGRID_C;
+  const int lr = lane >> 2, lc = lane & 3;
+  int stage = 0;
+  uint32_t phase = 0;
+  while (true) {
+    mbar_wait(ring.full0 + 8 * stage, phase);
+    const StageMeta& m = meta[stage];
+    if (m.flags & kEnd) break;
+    // first stage of a tile: balanced 2 x 2 warp split of its 8x8 blocks
+    const int tm = m.tm, tn = m.tn;
     const int mb = (tm + 7) >> 3, nb = (tn + 7) >> 3;
     const int mb0 = (mb + 1) >> 1, nb0 = (nb + 1) >> 1;
     const int mblk = wr == 0 ? mb0 : mb - mb0;
     const int nblk = wc == 0 ? nb0 : nb - nb0;
     const int wr0 = wr == 0 ? 0 : mb0 * 8;
     const int wc0 = wc == 0 ? 0 : nb0 * 8;
-    // fragment addresses per k4 step (bytes within a stage)
-    uint32_t fa[4], fb[4];
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      fa[ks] = TA ? ((4 * ks + lc) * (64 + PADN) + wr0 + lr) * 8
-                  : kc_pos(wr0 + lr, 4 * ks + lc) * 8;
-      fb[ks] = A_EL * 8 + (TB ? kc_pos(wc0 + lr, 4 * ks + lc) * 8
-                              : ((4 * ks + lc) * (64 + PADN) + wc0 + lr) * 8);
-    }
-    // row / col validity of this thread's 8 load elements
-    uint32_t amask = 0, bmask = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int ar = TA ? (tid % 64) : (tid / BK + 8 * i);
-      const int bc = TB ? (tid / BK + 8 * i) : (tid % 64);
-      amask |= (ar < tm ? 1u : 0u) << i;
-      bmask |= (bc < tn ? 1u : 0u) << i;
-    }
-
-    double acc[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-    const bool rows_full = amask == 0xffu && bmask == 0xffu;
-    int seg = prob.seg_begin;
-    SegState cur;
-    Seg nxt;  // raw descriptor of seg+1, loaded one segment ahead
-    if (seg < prob.seg_end) setup_seg<TA, TB>(cur, segs[seg], bases, tile.row0, tile.col0, tid);
-    if (seg + 1 < prob.seg_end) nxt = segs[seg + 1];
-    int nks0 = 0, nks1 = 0, nks2 = 0;
-    double sc0 = 0.0, sc1 = 0.0, sc2 = 0.0;
-
-    auto issue = [&](uint32_t sbase, int& nks_out, double& sc_out) {
-      if (seg < prob.seg_end) {
-        const int krem = min(BK, cur.kleft);
-        const uint32_t sa = sbase + sa_st, sb = sbase + sb_st;
-        if (krem == BK && rows_full) {
-          // full stage: no predicates, pointer-increment addressing
-#pragma unroll
-          for (int i = 0; i < 8; ++i) cp_async8_full(sa + i * sa_step, cur.a + i * cur.a_istep);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) cp_async8_full(sb + i * sb_step, cur.b + i * cur.b_istep);
-        } else {
-          // edge stage: skip rows outside the tile, zero-fill the k tail
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const bool kv = (TA ? a_k0 + 2 * i : a_k0) < krem;
-            if ((amask >> i) & 1u)
-              cp_async8(sa + i * sa_step, kv ? cur.a + i * cur.a_istep : cur.a, kv);
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const bool kv = (TB ? b_k0 : b_k0 + 2 * i) < krem;
-            if ((bmask >> i) & 1u)
-              cp_async8(sb + i * sb_step, kv ? cur.b + i * cur.b_istep : cur.b, kv);
-          }
-        }
-        nks_out = (krem + 3) >> 2;
-        sc_out = cur.scale;
-        cur.a += cur.a_k16;
-        cur.b += cur.b_k16;
-        cur.kleft -= BK;
-        if (cur.kleft <= 0) {
-          ++seg;
-          if (seg < prob.seg_end) setup_seg<TA, TB>(cur, nxt, bases, tile.row0, tile.col0, tid);
-          if (seg + 1 < prob.seg_end) nxt = segs[seg + 1];
-        }
-      } else {
-        nks_out = 0;
-        sc_out = 0.0;
-      }
-      cp_async_commit();
-    };
-
-    issue(smem_base, nks0, sc0);
-    issue(smem_base + STAGE_B, nks1, sc1);
-    uint32_t st_cur = smem_base;                 // stage being computed
-    uint32_t st_nxt = smem_base + 2 * STAGE_B;   // stage being filled
-    for (;;) {
-      cp_async_wait<STAGES - 2>();
-      __syncthreads();
-      if (nks0 == 0) break;
-      const int nks = nks0;
-      const double sc = sc0;
-      issue(st_nxt, nks2, sc2);
-      uint32_t a_ks[4], b_ks[4];
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        a_ks[ks] = st_cur + fa[ks];
-        b_ks[ks] = st_cur + fb[ks];
-      }
-      mma_dispatch<TA, TB>(acc, a_ks, b_ks, mblk, nblk, nks, sc);
-      nks0 = nks1;
-      sc0 = sc1;
-      nks1 = nks2;
-      sc1 = sc2;
-      st_cur = st_cur + STAGE_B == smem_base + STAGES * STAGE_B ? smem_base : st_cur + STAGE_B;
-      st_nxt = st_nxt + STAGE_B == smem_base + STAGES * STAGE_B ? smem_base : st_nxt + STAGE_B;
-    }
-    cp_async_wait<0>();
-
-    // ---- epilogue: masked store (optionally accumulating)
-    double* c = const_cast<double*>(resolve(bases, prob.c));
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = wr0 + i * 8 + lr;
-      if (i < mblk && row < tm) {
-        double* crow = c + (int64_t)(tile.row0 + row) * prob.ldc + tile.col0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int col = wc0 + j * 8 + lc * 2;
-          if (j < nblk) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (col + h < tn) {
-                double v = acc[i][j][h];
-                if (prob.beta) v += crow[col + h];
-                crow[col + h] = v;
-              }
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();  // s_tile visible; smem ring free for the next tile
-    t = s_tile[flip ^ 1];
-    flip ^= 1;
+    const uint32_t a_off = TA ? (lc * NC_LD + wr0 + lr) * 8 : kc_pos(wr0 + lr, lc) * 8;
+    const uint32_t b_off = A_EL * 8 + (TB ? kc_pos(wc0 + lr, lc) * 8 : (lc * NC_LD + wc0 + lr) * 8);
+    double* c = m.c + (int64_t)(wr0 + lr) * m.ldc + wc0 + 2 * lc;
+    consume_dispatch<TA, TB>(mblk, nblk, ring, stage, phase, a_off, b_off, lr & 3, c, m.ldc, m.beta,
+                             tm - wr0 - lr, tn - wc0 - 2 * lc, lane);
   }
 }
 

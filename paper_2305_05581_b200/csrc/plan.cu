@@ -53,20 +53,41 @@ struct Term {
   double coef;
 };
 
+// Host staging + device copy of one combine launch (combine.cuh).
+struct CombList {
+  std::vector<CombTask> tasks;
+  std::vector<CombOut> outs;
+  std::vector<CombTerm> terms;
+  CombTask* d_tasks = nullptr;
+  CombOut* d_outs = nullptr;
+  CombTerm* d_terms = nullptr;
+  int64_t ntasks = 0;
+  // chunk the elements of outputs [first, outs.size()) of n elements each
+  void add_tasks(int32_t first, int n) {
+    const int32_t last = static_cast<int32_t>(outs.size());
+    if (last > first)
+      for (int e0 = 0; e0 < n; e0 += COMB_CHUNK)
+        tasks.push_back({first, last, e0, std::min(COMB_CHUNK, n - e0)});
+  }
+  void release() {
+    if (d_tasks) cudaFree(d_tasks);
+    if (d_outs) cudaFree(d_outs);
+    if (d_terms) cudaFree(d_terms);
+    d_tasks = nullptr;
+    d_outs = nullptr;
+    d_terms = nullptr;
+  }
+};
+
 struct Chunk {
   GemmBatch host1, host2;  // released after upload
   DeviceBatch p1, p2;
-  std::vector<CombTask> ctasks;
-  std::vector<CombOut> couts;
-  std::vector<CombTerm> cterms;
-  CombTask* d_ctasks = nullptr;
-  CombOut* d_couts = nullptr;
-  CombTerm* d_cterms = nullptr;
-  int64_t nctasks = 0;
+  CombList comb0;          // phase 0: pre-summed left operators
+  CombList comb3;          // phase 3: split-K partial sums into σ
   int64_t ws_doubles = 0;
   int64_t flops0 = 0, flops1 = 0, flops2 = 0;
-  int64_t bytes0 = 0;
-  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  int64_t bytes0 = 0, bytes3 = 0;
+  cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
 }  // namespace
@@ -151,6 +172,14 @@ int upload_vec(const std::vector<T>& v, T** out) {
     rc = cuda_check(cudaMemcpy(*out, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice),
                     "upload combine list");
   return rc;
+}
+
+int launch_combine(const CombList& cl, const Bases& bases, cudaStream_t stream) {
+  if (cl.ntasks == 0) return SDMRG_OK;
+  combine_kernel<<<static_cast<unsigned>(cl.ntasks), COMB_THREADS, 0, stream>>>(
+      cl.d_tasks, cl.d_outs, cl.d_terms, bases);
+  count_launch();
+  return cuda_check(cudaGetLastError(), "combine_kernel launch");
 }
 
 }  // namespace
@@ -443,48 +472,107 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       if (!mine[i]) continue;
       for (const Pair& pr : pairs[i]) by_out[pr.out].push_back({i, &pr});
     }
+    struct OutProb {
+      int32_t o;
+      int q, r;
+      int64_t ksum;
+      std::vector<Seg> segs;
+    };
+    std::vector<OutProb> outs;
+    outs.reserve(by_out.size());
     for (auto& kv : by_out) {
       const int32_t o = kv.first;
       const int q = d->dim_l[keys[o].jl], r = d->dim_r[keys[o].jr];
-      ch.host2.begin_prob(make_handle(B_SIGMA, plan->offs[o]), r, q, r, 1);
+      OutProb op{o, q, r, 0, {}};
       for (size_t u = 0; u < kv.second.size();) {
         const int64_t i = kv.second[u].first;
         const int m = d->dim_l[keys[i].jl];
         const int qm = q * m;
-        const int32_t out_first = static_cast<int32_t>(ch.couts.size());
+        const int32_t out_first = static_cast<int32_t>(ch.comb0.outs.size());
         for (; u < kv.second.size() && kv.second[u].first == i; ++u) {
           const Pair& pr = *kv.second[u].second;
           const Term* tt = terms[i].data();
           const auto& th = tmap[i - i0].at(pr.rop);
+          Seg sg{};
+          sg.b = th.first;
+          sg.ldb = th.second;
+          sg.lda = m;
+          sg.k = m;
           if (pr.term_end - pr.term_begin == 1) {
             const Term& t = tt[pr.term_begin];
-            ch.host2.add_seg(make_handle(B_ARENA_L, d->blk_off_l[(int64_t)t.lop * nL + keys[i].jl]),
-                             m, th.first, th.second, m, t.coef);
+            sg.a = make_handle(B_ARENA_L, d->blk_off_l[(int64_t)t.lop * nL + keys[i].jl]);
+            sg.scale = t.coef;
           } else {
-            CombOut co{make_handle(B_WS, ws), static_cast<int32_t>(ch.cterms.size()), 0};
+            CombOut co{make_handle(B_WS, ws), static_cast<int32_t>(ch.comb0.terms.size()), 0};
             for (int32_t x = pr.term_begin; x < pr.term_end; ++x)
-              ch.cterms.push_back(
+              ch.comb0.terms.push_back(
                   {make_handle(B_ARENA_L, d->blk_off_l[(int64_t)tt[x].lop * nL + keys[i].jl]),
                    tt[x].coef});
-            co.term_end = static_cast<int32_t>(ch.cterms.size());
-            ch.couts.push_back(co);
-            ch.host2.add_seg(make_handle(B_WS, ws), m, th.first, th.second, m, 1.0);
+            co.term_end = static_cast<int32_t>(ch.comb0.terms.size());
+            ch.comb0.outs.push_back(co);
+            sg.a = make_handle(B_WS, ws);
+            sg.scale = 1.0;
             ws += qm;
             ch.flops0 += 2LL * (co.term_end - co.term_begin) * qm;
             ch.bytes0 += 8LL * (co.term_end - co.term_begin + 1) * qm;
             ++comb_outputs;
             comb_terms += co.term_end - co.term_begin;
           }
+          op.segs.push_back(sg);
+          op.ksum += m;
           exec_flops += 2LL * q * r * m;
           ch.flops2 += 2LL * q * r * m;
           ++products;
         }
-        const int32_t out_last = static_cast<int32_t>(ch.couts.size());
-        if (out_last > out_first)
-          for (int e0 = 0; e0 < qm; e0 += COMB_CHUNK)
-            ch.ctasks.push_back({out_first, out_last, e0, std::min(COMB_CHUNK, qm - e0)});
+        ch.comb0.add_tasks(out_first, qm);
       }
-      ch.host2.end_prob();
+      outs.push_back(std::move(op));
+    }
+    // split-K for load balance: a σ tile whose K work exceeds the granule
+    // (1/6 of one persistent CTA's share) is cut into contiguous segment
+    // ranges written to partial buffers; phase 3 adds them to σ in order
+    // (σ first, then parts 0..S-1: deterministic, no atomics).
+    auto tiles_of = [](int extent) { return (extent + BM - 1) / BM; };
+    double total_cost = 0.0;
+    for (const OutProb& op : outs) total_cost += double(op.q) * op.r * op.ksum;
+    const double granule =
+        total_cost / (double(d->dry_run ? 1 : engine_grid(false, false)) * 6.0) + 1.0;
+    for (const OutProb& op : outs) {
+      const double tile_cost =
+          double(op.q) / tiles_of(op.q) * (double(op.r) / tiles_of(op.r)) * op.ksum;
+      int nsplit = static_cast<int>(std::min<double>(std::ceil(tile_cost / granule),
+                                                     double(op.segs.size())));
+      nsplit = std::max(nsplit, 1);
+      const uint64_t sig = make_handle(B_SIGMA, plan->offs[op.o]);
+      if (nsplit == 1) {
+        ch.host2.begin_prob(sig, op.r, op.q, op.r, 1);
+        for (const Seg& sg : op.segs) ch.host2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale);
+        ch.host2.end_prob();
+        continue;
+      }
+      const int64_t qr = (int64_t)op.q * op.r;
+      const int32_t out_first = static_cast<int32_t>(ch.comb3.outs.size());
+      CombOut co{sig, static_cast<int32_t>(ch.comb3.terms.size()), 0};
+      ch.comb3.terms.push_back({sig, 1.0});
+      size_t u = 0;
+      int64_t kdone = 0;
+      for (int sp = 0; sp < nsplit && u < op.segs.size(); ++sp) {
+        const int64_t kcut = op.ksum * (sp + 1) / nsplit;
+        const uint64_t part = make_handle(B_WS, ws);
+        ch.host2.begin_prob(part, op.r, op.q, op.r, 0);
+        do {
+          const Seg& sg = op.segs[u++];
+          ch.host2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale);
+          kdone += sg.k;
+        } while (u < op.segs.size() && (kdone < kcut || sp == nsplit - 1));
+        ch.host2.end_prob();
+        ch.comb3.terms.push_back({part, 1.0});
+        ws += qr;
+      }
+      co.term_end = static_cast<int32_t>(ch.comb3.terms.size());
+      ch.comb3.outs.push_back(co);
+      ch.comb3.add_tasks(out_first, static_cast<int>(qr));
+      ch.bytes3 += 8LL * (co.term_end - co.term_begin + 1) * qr;
     }
     ch.host1.finalize_tiles();
     ch.host2.finalize_tiles();
@@ -506,15 +594,17 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     if (rc) break;
     rc = ch.host1.upload(&ch.p1, 0);
     if (!rc) rc = ch.host2.upload(&ch.p2, 0);
-    if (!rc) rc = upload_vec(ch.ctasks, &ch.d_ctasks);
-    if (!rc) rc = upload_vec(ch.couts, &ch.d_couts);
-    if (!rc) rc = upload_vec(ch.cterms, &ch.d_cterms);
-    ch.nctasks = static_cast<int64_t>(ch.ctasks.size());
+    for (CombList* cl : {&ch.comb0, &ch.comb3}) {
+      if (!rc) rc = upload_vec(cl->tasks, &cl->d_tasks);
+      if (!rc) rc = upload_vec(cl->outs, &cl->d_outs);
+      if (!rc) rc = upload_vec(cl->terms, &cl->d_terms);
+      cl->ntasks = static_cast<int64_t>(cl->tasks.size());
+      cl->tasks = std::vector<CombTask>();
+      cl->outs = std::vector<CombOut>();
+      cl->terms = std::vector<CombTerm>();
+    }
     ch.host1 = GemmBatch();
     ch.host2 = GemmBatch();
-    ch.ctasks = std::vector<CombTask>();
-    ch.couts = std::vector<CombOut>();
-    ch.cterms = std::vector<CombTerm>();
   }
   if (rc) {
     sdmrg_plan_destroy(plan);
@@ -535,7 +625,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   st.workspace_doubles = ws_max;
   int64_t kernels = 0;
   for (auto& ch : plan->chunks)
-    kernels += (ch.nctasks > 0) + (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0);
+    kernels += (ch.comb0.ntasks > 0) + (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0) +
+               (ch.comb3.ntasks > 0);
   st.kernels_per_apply = kernels;
   st.algo_bytes = static_cast<int64_t>(algo_bytes);
   st.products = products;
@@ -593,13 +684,8 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
   for (size_t c = 0; c < plan->chunks.size(); ++c) {
     Chunk& ch = plan->chunks[c];
     if (plan->timing) cudaEventRecord(ch.ev[0], stream);
-    if (ch.nctasks > 0) {
-      combine_kernel<<<static_cast<unsigned>(ch.nctasks), COMB_THREADS, 0, stream>>>(
-          ch.d_ctasks, ch.d_couts, ch.d_cterms, bases);
-      count_launch();
-      rc = cuda_check(cudaGetLastError(), "combine_kernel launch");
-      if (rc) return rc;
-    }
+    rc = launch_combine(ch.comb0, bases, stream);
+    if (rc) return rc;
     if (plan->timing) {
       cudaEventRecord(ch.ev[1], stream);
       cudaEventRecord(ch.ev[2], stream);
@@ -612,7 +698,13 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     }
     rc = launch_engine(false, false, ch.p2, bases, plan->counters + 2 * c + 1, stream);
     if (rc) return rc;
-    if (plan->timing) cudaEventRecord(ch.ev[5], stream);
+    if (plan->timing) {
+      cudaEventRecord(ch.ev[5], stream);
+      cudaEventRecord(ch.ev[6], stream);
+    }
+    rc = launch_combine(ch.comb3, bases, stream);
+    if (rc) return rc;
+    if (plan->timing) cudaEventRecord(ch.ev[7], stream);
   }
   return SDMRG_OK;
 }
@@ -632,13 +724,12 @@ int sdmrg_plan_set_timing(sdmrg_plan* plan, int enable) {
 
 int sdmrg_plan_timing(sdmrg_plan* plan, double* ms, int64_t* flops, int64_t* bytes) {
   if (!plan || !plan->timing) return fail(SDMRG_EINVAL, "plan_timing: timing not enabled");
-  double t[3] = {0.0, 0.0, 0.0};
-  int64_t f[3] = {0, 0, 0};
-  int64_t by = 0;
+  double t[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t f[4] = {0, 0, 0, 0}, by[4] = {0, 0, 0, 0};
   for (auto& ch : plan->chunks) {
-    int rc = cuda_check(cudaEventSynchronize(ch.ev[5]), "timing sync");
+    int rc = cuda_check(cudaEventSynchronize(ch.ev[7]), "timing sync");
     if (rc) return rc;
-    for (int p = 0; p < 3; ++p) {
+    for (int p = 0; p < 4; ++p) {
       float x = 0.f;
       cudaEventElapsedTime(&x, ch.ev[2 * p], ch.ev[2 * p + 1]);
       t[p] += x;
@@ -646,15 +737,13 @@ int sdmrg_plan_timing(sdmrg_plan* plan, double* ms, int64_t* flops, int64_t* byt
     f[0] += ch.flops0;
     f[1] += ch.flops1;
     f[2] += ch.flops2;
-    by += ch.bytes0;
+    by[0] += ch.bytes0;
+    by[3] += ch.bytes3;
   }
-  for (int p = 0; p < 3; ++p) {
+  for (int p = 0; p < 4; ++p) {
     if (ms) ms[p] = t[p];
     if (flops) flops[p] = f[p];
-  }
-  if (bytes) {
-    bytes[0] = by;
-    bytes[1] = bytes[2] = 0;
+    if (bytes) bytes[p] = by[p];
   }
   return SDMRG_OK;
 }
@@ -664,9 +753,8 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
   for (auto& ch : plan->chunks) {
     ch.p1.release();
     ch.p2.release();
-    if (ch.d_ctasks) cudaFree(ch.d_ctasks);
-    if (ch.d_couts) cudaFree(ch.d_couts);
-    if (ch.d_cterms) cudaFree(ch.d_cterms);
+    ch.comb0.release();
+    ch.comb3.release();
     for (auto& e : ch.ev)
       if (e) cudaEventDestroy(e);
   }

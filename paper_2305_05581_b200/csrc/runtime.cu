@@ -50,10 +50,8 @@ int engine_grid(bool ta, bool tb) {
 
 void DeviceBatch::release() {
   if (tiles) cudaFree(tiles);
-  if (probs) cudaFree(probs);
   if (segs) cudaFree(segs);
   tiles = nullptr;
-  probs = nullptr;
   segs = nullptr;
   ntiles = nprobs = nsegs = 0;
 }
@@ -131,41 +129,39 @@ int GemmBatch::upload(DeviceBatch* out, cudaStream_t stream) const {
   out->release();
   int rc;
   if (!tiles.empty()) {
-    if ((rc = cuda_check(cudaMalloc(&out->tiles, tiles.size() * sizeof(Tile)), "cudaMalloc tiles")))
+    std::vector<TileRec> recs(tiles.size());
+    for (size_t i = 0; i < tiles.size(); ++i) {
+      const Tile& t = tiles[i];
+      const Prob& p = probs[t.prob];
+      recs[i] = TileRec{p.c, p.ldc, p.beta, p.seg_begin, p.seg_end, t.row0, t.col0, t.tm, t.tn, 0};
+    }
+    if ((rc = cuda_check(cudaMalloc(&out->tiles, recs.size() * sizeof(TileRec)), "cudaMalloc tiles")))
       return rc;
-    if ((rc = cuda_check(cudaMemcpyAsync(out->tiles, tiles.data(), tiles.size() * sizeof(Tile),
-                                         cudaMemcpyHostToDevice, stream),
+    if ((rc = cuda_check(cudaMemcpy(out->tiles, recs.data(), recs.size() * sizeof(TileRec),
+                                    cudaMemcpyHostToDevice),
                          "upload tiles")))
-      return rc;
-  }
-  if (!probs.empty()) {
-    if ((rc = cuda_check(cudaMalloc(&out->probs, probs.size() * sizeof(Prob)), "cudaMalloc probs")))
-      return rc;
-    if ((rc = cuda_check(cudaMemcpyAsync(out->probs, probs.data(), probs.size() * sizeof(Prob),
-                                         cudaMemcpyHostToDevice, stream),
-                         "upload probs")))
       return rc;
   }
   if (!segs.empty()) {
     if ((rc = cuda_check(cudaMalloc(&out->segs, segs.size() * sizeof(Seg)), "cudaMalloc segs")))
       return rc;
-    if ((rc = cuda_check(cudaMemcpyAsync(out->segs, segs.data(), segs.size() * sizeof(Seg),
-                                         cudaMemcpyHostToDevice, stream),
+    if ((rc = cuda_check(cudaMemcpy(out->segs, segs.data(), segs.size() * sizeof(Seg),
+                                    cudaMemcpyHostToDevice),
                          "upload segs")))
       return rc;
   }
   out->ntiles = static_cast<int64_t>(tiles.size());
   out->nprobs = static_cast<int64_t>(probs.size());
   out->nsegs = static_cast<int64_t>(segs.size());
-  // the host vectors may die right after this call: make the copies complete
-  return cuda_check(cudaStreamSynchronize(stream), "upload sync");
+  (void)stream;
+  return SDMRG_OK;
 }
 
 template <bool TA, bool TB>
 static void launch_t(const DeviceBatch& b, const Bases& bases, int* counter, cudaStream_t stream) {
   const int grid = std::min<int64_t>(grid_for<TA, TB>(), std::max<int64_t>(b.ntiles, 1));
   seg_gemm_kernel<TA, TB><<<grid, THREADS, smem_bytes<TA, TB>(), stream>>>(
-      b.tiles, static_cast<int>(b.ntiles), b.probs, b.segs, counter, bases);
+      b.tiles, static_cast<int>(b.ntiles), b.segs, counter, bases);
 }
 
 int launch_engine(bool ta, bool tb, const DeviceBatch& b, const Bases& bases, int* counter,

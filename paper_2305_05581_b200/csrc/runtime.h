@@ -21,8 +21,7 @@ int engine_grid(bool ta, bool tb);
 
 // Device-side copy of a descriptor list.
 struct DeviceBatch {
-  Tile* tiles = nullptr;
-  Prob* probs = nullptr;
+  TileRec* tiles = nullptr;
   Seg* segs = nullptr;
   int64_t ntiles = 0, nprobs = 0, nsegs = 0;
   void release();

@@ -178,10 +178,11 @@ class DevicePlan:
 
     def last_timing(self):
         """Per-phase device ms, executed FLOPs and algorithmic bytes of the last
-        apply: phase 0 left-operator pre-summation, 1 T = A R^T, 2 σ += Lsum T."""
-        ms = (ctypes.c_double * 3)()
-        fl = (ctypes.c_int64 * 3)()
-        by = (ctypes.c_int64 * 3)()
+        apply: phase 0 left-operator pre-summation, 1 T = A R^T, 2 σ += Lsum T,
+        3 split-K partial sums into σ."""
+        ms = (ctypes.c_double * 4)()
+        fl = (ctypes.c_int64 * 4)()
+        by = (ctypes.c_int64 * 4)()
         _lib.check(_lib.load().sdmrg_plan_timing(self._h, ms, fl, by))
         return list(ms), list(fl), list(by)
 

@@ -19,11 +19,11 @@ res = [None] * 3
 for _ in range(3):
     plan.apply(psi, out)
     res[_] = plan.last_timing()
-ms = [min(r[0][k] for r in res) for k in range(3)]
+ms = [min(r[0][k] for r in res) for k in range(4)]
 fl, by = res[0][1], res[0][2]
 print(json.dumps({"lib": os.environ.get("SDMRG_LIB", "default"), "L": L, "D": D,
                   "ms": [round(x, 2) for x in ms],
-                  "tflops": [round(f / max(m, 1e-9) / 1e9, 2) for f, m in zip(fl, ms)],
-                  "combine_GBs": round(by[0] / max(ms[0], 1e-9) / 1e6, 1),
+                  "tflops": [round(f / max(m, 1e-9) / 1e9, 2) for f, m in zip(fl[1:3], ms[1:3])],
+                  "combine_GBs": [round(by[k] / max(ms[k], 1e-9) / 1e6, 1) for k in (0, 3)],
                   "total_ms": round(sum(ms), 2),
                   "ref_tflops": round(plan.stats["ref_flops"] / sum(ms) / 1e9, 2)}))
