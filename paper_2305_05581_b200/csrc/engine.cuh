@@ -222,7 +222,11 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
     const uint32_t a0 = ring.smem + stage * STAGE_B + a_off;
     const uint32_t b0 = ring.smem + stage * STAGE_B + b_off;
     if (MB > 0 && NB > 0) {
+#ifdef SDMRG_EXP_NOSCALE
+      const bool scaled = false;
+#else
       const bool scaled = scale != 1.0;
+#endif
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
         if (ks < nks) {
@@ -242,10 +246,12 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
               for (int i = 0; i < MB; ++i) af[i] *= scale;
             }
           }
+#ifndef SDMRG_EXP_NOMMA
 #pragma unroll
           for (int i = 0; i < MB; ++i)
 #pragma unroll
             for (int j = 0; j < NB; ++j) dmma(acc[i][j], af[i], bf[j]);
+#endif
         }
       }
     }
@@ -349,6 +355,40 @@ __device__ __forceinline__ void load_operand(uint32_t sbase, const double* src, 
   }
 }
 
+// L2 prefetch of one contiguous element range with a single bulk (TMA-unit)
+// prefetch: the range is widened to 16-byte alignment.
+__device__ __forceinline__ void bulk_prefetch_l2(const double* first, const double* last) {
+  const uint64_t lo = reinterpret_cast<uint64_t>(first) & ~uint64_t(15);
+  const uint64_t hi = (reinterpret_cast<uint64_t>(last) + 8 + 15) & ~uint64_t(15);
+  uint64_t n = hi - lo;
+  // one instruction moves at most 2^32 - 16 bytes; panels are far smaller
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(lo), "r"((uint32_t)n)
+               : "memory");
+}
+
+// Prefetch both operand panels of segment sg for the tile (row0, col0, tm,
+// tn) into L2: each panel of a row-major sector block is one address range.
+template <bool TA, bool TB>
+__device__ __forceinline__ void prefetch_segment(const Seg& sg, const TileRec& tr,
+                                                 double* const* sbases) {
+  const double* a = sbases[sg.a >> kHandleShift] + (sg.a & kHandleMask);
+  const double* b = sbases[sg.b >> kHandleShift] + (sg.b & kHandleMask);
+  if (TA) {
+    const double* p = a + tr.row0;
+    bulk_prefetch_l2(p, p + (int64_t)(sg.k - 1) * sg.lda + tr.tm - 1);
+  } else {
+    const double* p = a + (int64_t)tr.row0 * sg.lda;
+    bulk_prefetch_l2(p, p + (int64_t)(tr.tm - 1) * sg.lda + sg.k - 1);
+  }
+  if (TB) {
+    const double* p = b + (int64_t)tr.col0 * sg.ldb;
+    bulk_prefetch_l2(p, p + (int64_t)(tr.tn - 1) * sg.ldb + sg.k - 1);
+  } else {
+    const double* p = b + tr.col0;
+    bulk_prefetch_l2(p, p + (int64_t)(sg.k - 1) * sg.ldb + tr.tn - 1);
+  }
+}
+
 template <bool TA, bool TB>
 __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restrict__ tiles,
                                         int ntiles, const Seg* __restrict__ segs,
@@ -406,8 +446,19 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
     bool first = true;
     for (int s = cur.seg_begin; s < cur.seg_end; ++s) {
       const Seg sg = sn;
-      if (s + 1 < cur.seg_end) sn = segs[s + 1];
-      else if (next < ntiles && nrec.seg_begin < nrec.seg_end) sn = segs[nrec.seg_begin];
+      // optional: bulk-prefetch the next segment's panels into L2 (measured
+      // slower at L=30 D=2048: 111 -> 129 ms, profiles/r1_notes.md)
+      if (s + 1 < cur.seg_end) {
+        sn = segs[s + 1];
+#ifdef SDMRG_L2_PREFETCH
+        if (lane == 0) prefetch_segment<TA, TB>(sn, cur, sbases);
+#endif
+      } else if (next < ntiles && nrec.seg_begin < nrec.seg_end) {
+        sn = segs[nrec.seg_begin];
+#ifdef SDMRG_L2_PREFETCH
+        if (lane == 0) prefetch_segment<TA, TB>(sn, nrec, sbases);
+#endif
+      }
       const double* a = sbases[sg.a >> kHandleShift] + (sg.a & kHandleMask);
       const double* b = sbases[sg.b >> kHandleShift] + (sg.b & kHandleMask);
       // operand origins at this tile: A rows row0.., B cols col0..

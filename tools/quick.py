@@ -9,7 +9,8 @@ L = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 D = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
 pi = synthetic_plan_input(L, D)
 al, ar = fill_arenas_device(pi)
-plan = DevicePlan(pi, arena_l=al, arena_r=ar)
+ws = int(os.environ.get("SDMRG_WS", "0"))
+plan = DevicePlan(pi, arena_l=al, arena_r=ar, workspace_doubles=ws)
 psi = torch.randn(plan.psi_size, dtype=torch.float64, device="cuda")
 out = plan.empty_vector()
 for _ in range(2):
@@ -21,7 +22,8 @@ for _ in range(3):
     res[_] = plan.last_timing()
 ms = [min(r[0][k] for r in res) for k in range(4)]
 fl, by = res[0][1], res[0][2]
-print(json.dumps({"lib": os.environ.get("SDMRG_LIB", "default"), "L": L, "D": D,
+print(json.dumps({"lib": os.environ.get("SDMRG_LIB", "default"), "L": L, "D": D, "ws": ws,
+                  "chunks": plan.stats["chunks"],
                   "ms": [round(x, 2) for x in ms],
                   "tflops": [round(f / max(m, 1e-9) / 1e9, 2) for f, m in zip(fl[1:3], ms[1:3])],
                   "combine_GBs": [round(by[k] / max(ms[k], 1e-9) / 1e6, 1) for k in (0, 3)],
