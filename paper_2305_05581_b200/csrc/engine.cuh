@@ -24,12 +24,15 @@
 //   producer  pulls tiles from a global counter (one tile of lookahead, the
 //             next tile's descriptor and first segment prefetched), walks
 //             their segments and streams 16-deep K stages of both operands
-//             into a STAGES-deep shared-memory ring with 8-byte cp.async
-//             (sector blocks have odd leading dimensions: neither TMA nor
-//             16-byte copies apply).  Completion is signalled through
-//             mbarriers (cp.async.mbarrier.arrive.noinc), so descriptor and
-//             global-memory latency never stalls the math warps and the ring
-//             runs continuously across tile boundaries;
+//             into a STAGES-deep shared-memory ring, across tile boundaries.
+//             The H_eff plan keeps every operand block in a padded layout
+//             (even leading dimension, 16-byte aligned rows) so its loads are
+//             16-byte cp.async (LDGSTS.128); arbitrary user pointers
+//             (sdmrg_dgemm, sbmm4s, ...) take 8-byte cp.async.  Completion is
+//             tracked by mbarriers (cp.async.mbarrier.arrive.noinc), so
+//             descriptor and global-memory latency never stalls the math
+//             warps.  (One TMA-unit bulk copy per 128-byte operand row was
+//             measured 1.7x slower: profiles/r1_notes.md.)
 //   consumers a 2 x 2 warp grid over the tile's 8x8 blocks, balanced (a warp
 //             owns up to 4 x 4 blocks, 32 accumulators).  The (row blocks,
 //             col blocks) shape is dispatched once per tile into a
@@ -40,11 +43,10 @@
 // <= 183 in phase 2); a 128 x 128 CTA tile with 8 warps left each warp 8
 // DMMAs per k4 step on typical tiles and ran at 12-16 TFLOP/s (profiles/n4a).
 //
-// Shared-memory layouts per stage (doubles):
-//   K-contiguous operand tile [64][16], XOR-swizzled on 4-wide k groups:
-//       (r, k) -> r*16 + (((k>>2) ^ (r&3))<<2 | (k&3))
-//   M/N-contiguous operand tile [16][64+4] (padding): (k, r) -> k*68 + r
-// Both give conflict-free DMMA fragment loads (2 wavefronts per LDS.64).
+// Shared-memory layouts per stage (doubles), rows 16-byte aligned for bulk
+// copies and conflict-free for DMMA fragment loads (2 wavefronts per LDS.64):
+//   K-contiguous operand tile [64][16] with row stride 18: (r, k) -> r*18 + k
+//   M/N-contiguous operand tile [16][64+4]:                (k, r) -> k*68 + r
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -108,9 +110,9 @@ struct Seg {         // 40 B
 constexpr int BM = 64, BN = 64, BK = 16, STAGES = SDMRG_STAGES;
 constexpr int CONSUMERS = 4, WGRID_R = 2, WGRID_C = 2;
 constexpr int THREADS = 32 * (CONSUMERS + 1);
-constexpr int PADN = 4;                          // padding of M/N-contiguous tiles
-constexpr int KC_ELEMS = BM * BK;                // K-contiguous tile (BM == BN)
-constexpr int NC_LD = BM + PADN;
+constexpr int KC_LD = BK + 2;                    // K-contiguous row stride (144 B)
+constexpr int KC_ELEMS = BM * KC_LD;             // K-contiguous tile (BM == BN)
+constexpr int NC_LD = BM + 4;                    // M/N-contiguous row stride (544 B)
 constexpr int NC_ELEMS = BK * NC_LD;             // M/N-contiguous tile
 template <bool TA>
 __host__ __device__ constexpr int a_elems() { return TA ? NC_ELEMS : KC_ELEMS; }
@@ -144,11 +146,28 @@ __device__ __forceinline__ void cp_async8(uint32_t saddr, const double* gmem, bo
 __device__ __forceinline__ void cp_async8_full(uint32_t saddr, const double* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem));
 }
+// TMA-unit bulk copy global -> shared, completion counted in bytes on an mbarrier
+__device__ __forceinline__ void bulk_copy(uint32_t saddr, const double* gmem, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(saddr),
+      "l"(gmem), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void sts64_zero(uint32_t saddr) {
+  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(saddr), "d"(0.0) : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_cp_async(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
@@ -176,11 +195,6 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
   return v;
 }
 
-// swizzled position (in doubles) of element (r, k) in a K-contiguous tile
-__host__ __device__ constexpr int kc_pos(int r, int k) {
-  return r * BK + ((((k >> 2) ^ (r & 3)) << 2) | (k & 3));
-}
-
 // Shared state of one CTA's pipeline.
 struct Ring {
   uint32_t smem;     // shared address of stage 0
@@ -192,28 +206,21 @@ struct Ring {
 // ------------------------------------------------------------------ consumer
 // A warp owning MB x NB 8x8 blocks of a tile: runs every stage of the tile
 // (the first one already waited for), then the epilogue.  a_off/b_off: byte
-// offset of fragment (block 0, k4 step 0) within a stage; g = row & 3 of the
-// fragment rows (K-contiguous swizzle group).
+// offset of fragment (block 0, k4 step 0) within a stage.
 template <bool TA, bool TB, int MB, int NB>
 __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint32_t& phase,
-                                             uint32_t a_off, uint32_t b_off, int g, double* c,
-                                             int ldc, int beta, int row_lim, int col_lim,
-                                             int lane) {
+                                             uint32_t a_off, uint32_t b_off, double* c, int ldc,
+                                             int beta, int row_lim, int col_lim, int lane) {
   constexpr uint32_t STAGE_B = stage_elems<TA, TB>() * 8;
-  constexpr int A_I = TA ? 8 * 8 : 8 * BK * 8;            // next 8-row block (bytes)
-  constexpr int B_J = TB ? 8 * BK * 8 : 8 * 8;            // next 8-col block
-  constexpr int NC_KS = 4 * NC_LD * 8;                    // next k4 step, M/N-contiguous
+  constexpr int A_I = TA ? 8 * 8 : 8 * KC_LD * 8;         // next 8-row block (bytes)
+  constexpr int B_J = TB ? 8 * KC_LD * 8 : 8 * 8;         // next 8-col block
+  constexpr int A_KS = TA ? 4 * NC_LD * 8 : 4 * 8;        // next k4 step
+  constexpr int B_KS = TB ? 4 * 8 : 4 * NC_LD * 8;
   double acc[MB > 0 ? MB : 1][NB > 0 ? NB : 1][2];
 #pragma unroll
   for (int i = 0; i < MB; ++i)
 #pragma unroll
     for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  // K-contiguous (swizzled) tiles: step ks of a fragment whose row has
-  // (row & 3) == g sits at 32-byte group (ks ^ g); the offsets already point
-  // at group g.
-  int ksw[4];
-#pragma unroll
-  for (int ks = 0; ks < 4; ++ks) ksw[ks] = ((ks ^ g) - g) << 5;
   while (true) {
     const StageMeta& m = ring.meta[stage];
     const int flags = m.flags;
@@ -232,11 +239,9 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
         if (ks < nks) {
           double af[MB > 0 ? MB : 1], bf[NB > 0 ? NB : 1];
 #pragma unroll
-          for (int i = 0; i < MB; ++i)
-            af[i] = lds64(TA ? a0 + ks * NC_KS + i * A_I : a0 + i * A_I + ksw[ks]);
+          for (int i = 0; i < MB; ++i) af[i] = lds64(a0 + ks * A_KS + i * A_I);
 #pragma unroll
-          for (int j = 0; j < NB; ++j)
-            bf[j] = lds64(TB ? b0 + j * B_J + ksw[ks] : b0 + ks * NC_KS + j * B_J);
+          for (int j = 0; j < NB; ++j) bf[j] = lds64(b0 + ks * B_KS + j * B_J);
           if (scaled) {
             if (NB <= MB) {
 #pragma unroll
@@ -285,16 +290,16 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
   }
 }
 
-#define SDMRG_TILE_CASE(MB, NB)                                                              \
-  case (MB) * 8 + (NB):                                                                      \
-    consume_tile<TA, TB, MB, NB>(ring, stage, phase, a_off, b_off, g, c, ldc, beta, row_lim, \
-                                 col_lim, lane);                                             \
+#define SDMRG_TILE_CASE(MB, NB)                                                                   \
+  case (MB) * 8 + (NB):                                                                           \
+    consume_tile<TA, TB, MB, NB>(ring, stage, phase, a_off, b_off, c, ldc, beta, row_lim, col_lim, \
+                                 lane);                                                           \
     break;
 
 template <bool TA, bool TB>
 __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring& ring, int& stage,
                                                  uint32_t& phase, uint32_t a_off, uint32_t b_off,
-                                                 int g, double* c, int ldc, int beta, int row_lim,
+                                                 double* c, int ldc, int beta, int row_lim,
                                                  int col_lim, int lane) {
   switch (mblk * 8 + nblk) {
     SDMRG_TILE_CASE(4, 4) SDMRG_TILE_CASE(4, 3) SDMRG_TILE_CASE(4, 2) SDMRG_TILE_CASE(4, 1)
@@ -302,38 +307,36 @@ __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring&
     SDMRG_TILE_CASE(2, 4) SDMRG_TILE_CASE(2, 3) SDMRG_TILE_CASE(2, 2) SDMRG_TILE_CASE(2, 1)
     SDMRG_TILE_CASE(1, 4) SDMRG_TILE_CASE(1, 3) SDMRG_TILE_CASE(1, 2) SDMRG_TILE_CASE(1, 1)
     default:  // no blocks for this warp: walk the tile's stages
-      consume_tile<TA, TB, 0, 0>(ring, stage, phase, a_off, b_off, g, c, ldc, beta, row_lim,
-                                 col_lim, lane);
+      consume_tile<TA, TB, 0, 0>(ring, stage, phase, a_off, b_off, c, ldc, beta, row_lim, col_lim,
+                                 lane);
       break;
   }
 }
 #undef SDMRG_TILE_CASE
 
 // ------------------------------------------------------------------ producer
-// Per-lane load geometry of one operand within a stage (one producer warp).
+// 8-byte cp.async geometry of one operand within a stage (one producer warp).
 //   K-contiguous (A when !TA, B when TB): lane -> k = lane & 15, rows
 //     (lane >> 4) + 2i, i < 32; element (r, k) at src + r*ld + k.
 //   M/N-contiguous: lane -> columns lane, lane + 32; k = 0..15; element
 //     (k, c) at src + k*ld + c.
+// The k tail beyond krem is zero-filled (stale shared memory may hold
+// non-finite data at kernel start).
 template <bool KCONTIG>
-__device__ __forceinline__ void load_operand(uint32_t sbase, const double* src, int ld, int extent,
-                                             int krem, int lane) {
+__device__ __forceinline__ void load_operand_async(uint32_t sbase, const double* src, int ld,
+                                                   int extent, int krem, int lane) {
   if (KCONTIG) {
     const int kk = lane & 15, r0 = lane >> 4;
     const double* p = src + (int64_t)r0 * ld + kk;
-    // rows r0 + 2i: (r & 3) alternates between r0 and r0 + 2
-    const uint32_t s_even = sbase + kc_pos(r0, kk) * 8;
-    const uint32_t s_odd = sbase + kc_pos(r0 + 2, kk) * 8 - 2 * BK * 8;
+    const uint32_t s0 = sbase + (r0 * KC_LD + kk) * 8;
     const int nrow = (extent - r0 + 1) >> 1;
     if (kk < krem) {
 #pragma unroll 8
       for (int i = 0; i < nrow; ++i)
-        cp_async8_full((i & 1 ? s_odd : s_even) + i * (2 * BK * 8), p + (int64_t)(2 * i) * ld);
+        cp_async8_full(s0 + i * (2 * KC_LD * 8), p + (int64_t)(2 * i) * ld);
     } else {
-      // zero-fill the k tail (stale shared memory may hold non-finite data)
 #pragma unroll 8
-      for (int i = 0; i < nrow; ++i)
-        cp_async8((i & 1 ? s_odd : s_even) + i * (2 * BK * 8), src, false);
+      for (int i = 0; i < nrow; ++i) cp_async8(s0 + i * (2 * KC_LD * 8), src, false);
     }
   } else {
 #pragma unroll
@@ -355,14 +358,62 @@ __device__ __forceinline__ void load_operand(uint32_t sbase, const double* src, 
   }
 }
 
+// 16-byte cp.async geometry (padded layouts: even leading dimensions, even
+// element offsets, so every element pair (k, k+1) / (c, c+1) is 16-byte
+// aligned in global and shared memory):
+//   K-contiguous: lane -> k pair kp = lane & 7 (k = 2kp, 2kp+1), rows
+//     (lane >> 3) + 4i, i < 16;
+//   M/N-contiguous: lane -> column pair (2 lane, 2 lane + 1), k = 0..15.
+// A pair straddling the k tail copies its first element and zero-fills the
+// second (src-size 8); pairs past the tail are zero-filled (src-size 0).
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const double* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async16_full(uint32_t saddr, const double* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
+}
+template <bool KCONTIG>
+__device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const double* src, int ld,
+                                                     int extent, int krem, int lane) {
+  if (KCONTIG) {
+    const int k = 2 * (lane & 7), r0 = lane >> 3;
+    const double* p = src + (int64_t)r0 * ld + k;
+    const uint32_t s0 = sbase + (r0 * KC_LD + k) * 8;
+    const int nrow = (extent - r0 + 3) >> 2;
+    if (k + 1 < krem) {
+#pragma unroll 4
+      for (int i = 0; i < nrow; ++i) cp_async16_full(s0 + i * (4 * KC_LD * 8), p + (int64_t)(4 * i) * ld);
+    } else {
+      const int bytes = k < krem ? 8 : 0;
+      const double* q = k < krem ? p : src;
+      const int64_t step = k < krem ? 4 * (int64_t)ld : 0;
+#pragma unroll 4
+      for (int i = 0; i < nrow; ++i) cp_async16(s0 + i * (4 * KC_LD * 8), q + i * step, bytes);
+    }
+  } else {
+    const int c = 2 * lane;
+    if (c < extent) {
+      const double* p = src + c;
+      const uint32_t s0 = sbase + c * 8;
+      if (krem >= BK) {
+#pragma unroll
+        for (int k = 0; k < BK; ++k) cp_async16_full(s0 + k * (NC_LD * 8), p + (int64_t)k * ld);
+      } else {
+#pragma unroll
+        for (int k = 0; k < BK; ++k)
+          cp_async16(s0 + k * (NC_LD * 8), k < krem ? p + (int64_t)k * ld : src, k < krem ? 16 : 0);
+      }
+    }
+  }
+}
+
 // L2 prefetch of one contiguous element range with a single bulk (TMA-unit)
 // prefetch: the range is widened to 16-byte alignment.
 __device__ __forceinline__ void bulk_prefetch_l2(const double* first, const double* last) {
   const uint64_t lo = reinterpret_cast<uint64_t>(first) & ~uint64_t(15);
   const uint64_t hi = (reinterpret_cast<uint64_t>(last) + 8 + 15) & ~uint64_t(15);
-  uint64_t n = hi - lo;
-  // one instruction moves at most 2^32 - 16 bytes; panels are far smaller
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(lo), "r"((uint32_t)n)
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(lo), "r"((uint32_t)(hi - lo))
                : "memory");
 }
 
@@ -389,15 +440,16 @@ __device__ __forceinline__ void prefetch_segment(const Seg& sg, const TileRec& t
   }
 }
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, bool BULK>
 __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restrict__ tiles,
                                         int ntiles, const Seg* __restrict__ segs,
                                         int* __restrict__ counter, double* const* sbases,
                                         int lane) {
   constexpr int A_EL = a_elems<TA>();
   constexpr uint32_t STAGE_B = stage_elems<TA, TB>() * 8;
-  auto publish = [&](int stage, int nks, double scale, int flags, const TileRec& tr,
-                     double* cptr) {
+  // lane 0 writes the stage metadata; the arrive publishes it (release)
+  auto meta_write = [&](int stage, int nks, double scale, int flags, const TileRec& tr,
+                        double* cptr) {
     if (lane == 0) {
       StageMeta& m = ring.meta[stage];
       m.nks = nks;
@@ -411,6 +463,9 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
         m.tn = tr.tn;
       }
     }
+  };
+  auto publish_empty = [&](int stage) {  // a stage without operand data
+    __syncwarp();
     mbar_arrive_cp_async(ring.full0 + 8 * stage);
     if (lane == 0) mbar_arrive(ring.full0 + 8 * stage);
   };
@@ -436,7 +491,8 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
     if (cur.seg_begin == cur.seg_end) {
       // no K at all: C = beta * C (one empty stage carries the epilogue)
       mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
-      publish(stage, 0, 1.0, kFirst | kLast, cur, cptr);
+      meta_write(stage, 0, 1.0, kFirst | kLast, cur, cptr);
+      publish_empty(stage);
       if (++stage == STAGES) {
         stage = 0;
         phase ^= 1;
@@ -446,8 +502,6 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
     bool first = true;
     for (int s = cur.seg_begin; s < cur.seg_end; ++s) {
       const Seg sg = sn;
-      // optional: bulk-prefetch the next segment's panels into L2 (measured
-      // slower at L=30 D=2048: 111 -> 129 ms, profiles/r1_notes.md)
       if (s + 1 < cur.seg_end) {
         sn = segs[s + 1];
 #ifdef SDMRG_L2_PREFETCH
@@ -469,14 +523,25 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
         mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
         const uint32_t sa = ring.smem + stage * STAGE_B;
         const uint32_t sb = sa + A_EL * 8;
-#ifndef SDMRG_EXP_NOLOAD
-        // A: K-contig iff !TA (element (r,k) at a + r*lda + k); B: K-contig iff TB
-        load_operand<!TA>(sa, TA ? a + (int64_t)k0 * sg.lda : a + k0, sg.lda, cur.tm, krem, lane);
-        load_operand<TB>(sb, TB ? b + k0 : b + (int64_t)k0 * sg.ldb, sg.ldb, cur.tn, krem, lane);
-#endif
+        const uint32_t full = ring.full0 + 8 * stage;
         const bool last = (s + 1 == cur.seg_end) && (k0 + BK >= sg.k);
-        publish(stage, (krem + 3) >> 2, sg.scale, (first ? kFirst : 0) | (last ? kLast : 0), cur,
-                cptr);
+        meta_write(stage, (krem + 3) >> 2, sg.scale, (first ? kFirst : 0) | (last ? kLast : 0),
+                   cur, cptr);
+        // A: K-contig iff !TA (element (r,k) at a + r*lda + k); B: K-contig iff TB
+        const double* asrc = TA ? a + (int64_t)k0 * sg.lda : a + k0;
+        const double* bsrc = TB ? b + k0 : b + (int64_t)k0 * sg.ldb;
+#ifndef SDMRG_EXP_NOLOAD
+        if (BULK) {
+          load_operand_aligned<!TA>(sa, asrc, sg.lda, cur.tm, krem, lane);
+          load_operand_aligned<TB>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
+        } else {
+          load_operand_async<!TA>(sa, asrc, sg.lda, cur.tm, krem, lane);
+          load_operand_async<TB>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
+        }
+#endif
+        __syncwarp();
+        mbar_arrive_cp_async(full);
+        if (lane == 0) mbar_arrive(full);
         first = false;
         if (++stage == STAGES) {
           stage = 0;
@@ -488,10 +553,14 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
     cur = nrec;
   }
   mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
-  publish(stage, 0, 1.0, kEnd, cur, nullptr);
+  meta_write(stage, 0, 1.0, kEnd, cur, nullptr);
+  publish_empty(stage);
 }
 
-template <bool TA, bool TB>
+// BULK ("aligned"): every operand block 16-byte aligned with even leading
+// dimensions (the H_eff plan's padded layouts) -> 16-byte cp.async; the
+// launcher selects it per batch.
+template <bool TA, bool TB, bool BULK>
 __global__ void __launch_bounds__(THREADS, SDMRG_MINB)
 seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __restrict__ segs,
                 int* __restrict__ counter, Bases bases) {
@@ -520,7 +589,7 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
   __syncthreads();
 
   if (warp == CONSUMERS) {
-    produce<TA, TB>(ring, tiles, ntiles, segs, counter, sbases, lane);
+    produce<TA, TB, BULK>(ring, tiles, ntiles, segs, counter, sbases, lane);
     return;
   }
 
@@ -541,10 +610,11 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
     const int nblk = wc == 0 ? nb0 : nb - nb0;
     const int wr0 = wr == 0 ? 0 : mb0 * 8;
     const int wc0 = wc == 0 ? 0 : nb0 * 8;
-    const uint32_t a_off = TA ? (lc * NC_LD + wr0 + lr) * 8 : kc_pos(wr0 + lr, lc) * 8;
-    const uint32_t b_off = A_EL * 8 + (TB ? kc_pos(wc0 + lr, lc) * 8 : (lc * NC_LD + wc0 + lr) * 8);
+    const uint32_t a_off = TA ? (lc * NC_LD + wr0 + lr) * 8 : ((wr0 + lr) * KC_LD + lc) * 8;
+    const uint32_t b_off =
+        A_EL * 8 + (TB ? ((wc0 + lr) * KC_LD + lc) * 8 : (lc * NC_LD + wc0 + lr) * 8);
     double* c = m.c + (int64_t)(wr0 + lr) * m.ldc + wc0 + 2 * lc;
-    consume_dispatch<TA, TB>(mblk, nblk, ring, stage, phase, a_off, b_off, lr & 3, c, m.ldc, m.beta,
+    consume_dispatch<TA, TB>(mblk, nblk, ring, stage, phase, a_off, b_off, c, m.ldc, m.beta,
                              tm - wr0 - lr, tn - wc0 - 2 * lc, lane);
   }
 }

@@ -34,7 +34,14 @@ using namespace sdmrg;
 
 namespace {
 
+// Engine bases.  The engine's bulk-copy producer needs 16-byte aligned
+// operand rows, so the plan keeps padded copies of everything it reads
+// (even leading dimensions, even element offsets, zero pads): the operator
+// arenas (repacked once at build), ψ (copied per apply) and the workspace.
+// σ is only written (epilogue) and keeps the reference layout.
 enum { B_PSI = 0, B_SIGMA = 1, B_ARENA_L = 2, B_ARENA_R = 3, B_WS = 4 };
+
+inline int pad2(int x) { return x + (x & 1); }
 
 struct Member {
   int32_t out;
@@ -51,6 +58,33 @@ struct Pair {
 struct Term {
   int32_t lop;
   double coef;
+};
+
+// Block copies into a padded layout (row stride change), one CTA per block.
+struct PadTask {
+  int64_t src, dst;      // element offsets
+  int32_t rows, cols;
+  int32_t src_ld, dst_ld;
+};
+__global__ void pad_kernel(const PadTask* __restrict__ tasks, int64_t n,
+                           const double* __restrict__ src, double* __restrict__ dst) {
+  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    const PadTask pt = tasks[t];
+    const int64_t count = (int64_t)pt.rows * pt.cols;
+    for (int64_t e = threadIdx.x; e < count; e += blockDim.x) {
+      const int64_t r = e / pt.cols, c = e - r * pt.cols;
+      dst[pt.dst + r * pt.dst_ld + c] = src[pt.src + r * pt.src_ld + c];
+    }
+  }
+}
+struct PadList {
+  PadTask* d_tasks = nullptr;
+  int64_t n = 0;
+  void release() {
+    if (d_tasks) cudaFree(d_tasks);
+    d_tasks = nullptr;
+    n = 0;
+  }
 };
 
 // Host staging + device copy of one combine launch (combine.cuh).
@@ -104,8 +138,11 @@ struct sdmrg_plan {
   std::vector<Chunk> chunks;
   double* workspace = nullptr;
   int* counters = nullptr;
-  const double* arena_l = nullptr;
-  const double* arena_r = nullptr;
+  double* arena_l = nullptr;       // padded device copies (owned)
+  double* arena_r = nullptr;
+  double* psi_pad = nullptr;       // padded ψ, refilled by every apply
+  std::vector<int64_t> poffs;      // padded ψ block offsets (psi_keys + 1)
+  PadList psi_copy;                // ψ -> psi_pad block list (device)
   sdmrg_plan_stats stats{};
   int timing = 0;
 };
@@ -197,8 +234,6 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   plan->nsite = ns;
   plan->nL = nL;
   plan->nR = nR;
-  plan->arena_l = d->arena_l;
-  plan->arena_r = d->arena_r;
 
   // ---- ψ keys (blocks.py:416-429): qR = target - qL - q1 - q2 ∈ right basis
   std::map<QN, int> rindex;
@@ -243,9 +278,36 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     psi_index[((size_t)k.jl * ns + k.s1) * ns + k.s2] = static_cast<int32_t>(i);
   }
   plan->offs[nk] = off;
+  plan->poffs.resize(nk + 1);
+  {
+    int64_t po = 0;
+    for (int64_t i = 0; i < nk; ++i) {
+      plan->poffs[i] = po;
+      po += (int64_t)d->dim_l[keys[i].jl] * pad2(d->dim_r[keys[i].jr]);
+    }
+    plan->poffs[nk] = po;
+  }
+  // padded arena offsets: block (op, column sector j) has rows dim(j + delta),
+  // row stride pad2(dim(j))
+  auto pad_offsets = [](int nops, int nsec, const int64_t* boff, const int32_t* shift,
+                        const int32_t* dim, std::vector<int64_t>& out) {
+    out.assign((size_t)nops * nsec, -1);
+    int64_t pos = 0;
+    for (int o = 0; o < nops; ++o)
+      for (int j = 0; j < nsec; ++j) {
+        const size_t x = (size_t)o * nsec + j;
+        if (boff[x] < 0 || shift[x] < 0) continue;
+        out[x] = pos;
+        pos += (int64_t)dim[shift[x]] * pad2(dim[j]);
+      }
+    return pos;
+  };
 
   const std::vector<int32_t> shL = shift_table(d->nops_l, d->delta_l, nL, d->qn_l, nc);
   const std::vector<int32_t> shR = shift_table(d->nops_r, d->delta_r, nR, d->qn_r, nc);
+  std::vector<int64_t> poff_l, poff_r;
+  const int64_t psize_l = pad_offsets(d->nops_l, nL, d->blk_off_l, shL.data(), d->dim_l, poff_l);
+  const int64_t psize_r = pad_offsets(d->nops_r, nR, d->blk_off_r, shR.data(), d->dim_r, poff_r);
 
   // ---- task generation: members per ψ key, rows in table order
   std::vector<std::vector<Member>> per_key(nk);
@@ -380,14 +442,14 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     std::vector<int32_t> rops;
     for (const Pair& p : pairs[i]) {
       rops.push_back(p.rop);
-      if (p.term_end - p.term_begin > 1) t_need[i] += (int64_t)d->dim_l[keys[p.out].jl] * m;
+      if (p.term_end - p.term_begin > 1) t_need[i] += (int64_t)d->dim_l[keys[p.out].jl] * pad2(m);
     }
     std::sort(rops.begin(), rops.end());
     rops.erase(std::unique(rops.begin(), rops.end()), rops.end());
     for (int32_t ro : rops) {
       if (d->kind_r[ro] == 1) continue;
       const int jrp = shR[(size_t)ro * nR + keys[i].jr];
-      t_need[i] += m * d->dim_r[jrp];
+      t_need[i] += m * pad2(d->dim_r[jrp]);
     }
   }
   int64_t total_t = 0;
@@ -448,17 +510,17 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
         const int ro = pr.rop;
         if (tm.count(ro)) continue;
         if (d->kind_r[ro] == 1) {  // R = identity: T = A (no product)
-          tm[ro] = {make_handle(B_PSI, plan->offs[i]), n};
+          tm[ro] = {make_handle(B_PSI, plan->poffs[i]), pad2(n)};
           continue;
         }
         const int jrp = shR[(size_t)ro * nR + k.jr];
         const int r = d->dim_r[jrp];
-        tm[ro] = {make_handle(B_WS, ws), r};
-        ch.host1.begin_prob(make_handle(B_WS, ws), r, m, r, 0);
-        ch.host1.add_seg(make_handle(B_PSI, plan->offs[i]), n,
-                         make_handle(B_ARENA_R, d->blk_off_r[(int64_t)ro * nR + k.jr]), n, n, 1.0);
+        tm[ro] = {make_handle(B_WS, ws), pad2(r)};
+        ch.host1.begin_prob(make_handle(B_WS, ws), pad2(r), m, r, 0);
+        ch.host1.add_seg(make_handle(B_PSI, plan->poffs[i]), pad2(n),
+                         make_handle(B_ARENA_R, poff_r[(size_t)ro * nR + k.jr]), pad2(n), n, 1.0);
         ch.host1.end_prob();
-        ws += (int64_t)m * r;
+        ws += (int64_t)m * pad2(r);
         exec_flops += 2LL * m * n * r;
         ch.flops1 += 2LL * m * n * r;
         ++t_problems;
@@ -487,7 +549,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       for (size_t u = 0; u < kv.second.size();) {
         const int64_t i = kv.second[u].first;
         const int m = d->dim_l[keys[i].jl];
-        const int qm = q * m;
+        const int qm = q * pad2(m);  // a padded q x m block, pads included
         const int32_t out_first = static_cast<int32_t>(ch.comb0.outs.size());
         for (; u < kv.second.size() && kv.second[u].first == i; ++u) {
           const Pair& pr = *kv.second[u].second;
@@ -496,17 +558,17 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
           Seg sg{};
           sg.b = th.first;
           sg.ldb = th.second;
-          sg.lda = m;
+          sg.lda = pad2(m);
           sg.k = m;
           if (pr.term_end - pr.term_begin == 1) {
             const Term& t = tt[pr.term_begin];
-            sg.a = make_handle(B_ARENA_L, d->blk_off_l[(int64_t)t.lop * nL + keys[i].jl]);
+            sg.a = make_handle(B_ARENA_L, poff_l[(size_t)t.lop * nL + keys[i].jl]);
             sg.scale = t.coef;
           } else {
             CombOut co{make_handle(B_WS, ws), static_cast<int32_t>(ch.comb0.terms.size()), 0};
             for (int32_t x = pr.term_begin; x < pr.term_end; ++x)
               ch.comb0.terms.push_back(
-                  {make_handle(B_ARENA_L, d->blk_off_l[(int64_t)tt[x].lop * nL + keys[i].jl]),
+                  {make_handle(B_ARENA_L, poff_l[(size_t)tt[x].lop * nL + keys[i].jl]),
                    tt[x].coef});
             co.term_end = static_cast<int32_t>(ch.comb0.terms.size());
             ch.comb0.outs.push_back(co);
@@ -567,7 +629,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
         } while (u < op.segs.size() && (kdone < kcut || sp == nsplit - 1));
         ch.host2.end_prob();
         ch.comb3.terms.push_back({part, 1.0});
-        ws += qr;
+        ws += qr + (qr & 1);
       }
       co.term_end = static_cast<int32_t>(ch.comb3.terms.size());
       ch.comb3.outs.push_back(co);
@@ -586,7 +648,59 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   int64_t ws_max = 0;
   for (auto& ch : plan->chunks) ws_max = std::max(ws_max, ch.ws_doubles);
   rc = SDMRG_OK;
-  if (ws_max > 0) rc = cuda_check(cudaMalloc(&plan->workspace, sizeof(double) * ws_max), "cudaMalloc workspace");
+  if (!d->dry_run) {
+    // padded device copies of the arenas and ψ; zeroed so every pad is 0
+    auto repack = [&](const double* src, const int64_t* boff, const std::vector<int64_t>& poff,
+                      const std::vector<int32_t>& shift, const int32_t* dim, int nops, int nsec,
+                      int64_t psize, double** out) {
+      int r = cuda_check(cudaMalloc(out, sizeof(double) * std::max<int64_t>(psize, 2)),
+                         "cudaMalloc padded arena");
+      if (!r) r = cuda_check(cudaMemset(*out, 0, sizeof(double) * std::max<int64_t>(psize, 2)),
+                             "memset padded arena");
+      std::vector<PadTask> tasks;
+      for (int o = 0; o < nops; ++o)
+        for (int j = 0; j < nsec; ++j) {
+          const size_t x = (size_t)o * nsec + j;
+          if (poff[x] < 0) continue;
+          tasks.push_back({boff[x], poff[x], dim[shift[x]], dim[j], dim[j], pad2(dim[j])});
+        }
+      PadList pl;
+      if (!r) r = upload_vec(tasks, &pl.d_tasks);
+      pl.n = static_cast<int64_t>(tasks.size());
+      if (!r && pl.n > 0) {
+        if (!src) r = fail(SDMRG_EINVAL, "plan: null operator arena");
+        else {
+          pad_kernel<<<static_cast<unsigned>(std::min<int64_t>(pl.n, 148 * 16)), 256>>>(
+              pl.d_tasks, pl.n, src, *out);
+          count_launch();
+          r = cuda_check(cudaDeviceSynchronize(), "repack arena");
+        }
+      }
+      pl.release();
+      return r;
+    };
+    rc = repack(d->arena_l, d->blk_off_l, poff_l, shL, d->dim_l, d->nops_l, nL, psize_l,
+                &plan->arena_l);
+    if (!rc)
+      rc = repack(d->arena_r, d->blk_off_r, poff_r, shR, d->dim_r, d->nops_r, nR, psize_r,
+                  &plan->arena_r);
+    const int64_t pp = std::max<int64_t>(plan->poffs[nk], 2);
+    if (!rc) rc = cuda_check(cudaMalloc(&plan->psi_pad, sizeof(double) * pp), "cudaMalloc psi_pad");
+    if (!rc) rc = cuda_check(cudaMemset(plan->psi_pad, 0, sizeof(double) * pp), "memset psi_pad");
+    std::vector<PadTask> ptasks;
+    for (int64_t i = 0; i < nk; ++i) {
+      const int m = d->dim_l[keys[i].jl], n = d->dim_r[keys[i].jr];
+      ptasks.push_back({plan->offs[i], plan->poffs[i], m, n, n, pad2(n)});
+    }
+    if (!rc) rc = upload_vec(ptasks, &plan->psi_copy.d_tasks);
+    plan->psi_copy.n = static_cast<int64_t>(ptasks.size());
+  }
+  if (!rc && ws_max > 0) {
+    rc = cuda_check(cudaMalloc(&plan->workspace, sizeof(double) * ws_max), "cudaMalloc workspace");
+    // T pads are never written by the engine: zero them once
+    if (!rc) rc = cuda_check(cudaMemset(plan->workspace, 0, sizeof(double) * ws_max),
+                             "memset workspace");
+  }
   if (!rc && !plan->chunks.empty())
     rc = cuda_check(cudaMalloc(&plan->counters, sizeof(int) * 2 * plan->chunks.size()),
                     "cudaMalloc counters");
@@ -675,8 +789,15 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
   rc = cuda_check(cudaMemsetAsync(plan->counters, 0, sizeof(int) * 2 * plan->chunks.size(), stream),
                   "memset counters");
   if (rc) return rc;
+  if (plan->psi_copy.n > 0) {
+    pad_kernel<<<static_cast<unsigned>(std::min<int64_t>(plan->psi_copy.n, 148 * 8)), 256, 0,
+                 stream>>>(plan->psi_copy.d_tasks, plan->psi_copy.n, psi, plan->psi_pad);
+    count_launch();
+    rc = cuda_check(cudaGetLastError(), "psi pad launch");
+    if (rc) return rc;
+  }
   Bases bases{};
-  bases.p[B_PSI] = const_cast<double*>(psi);
+  bases.p[B_PSI] = plan->psi_pad;
   bases.p[B_SIGMA] = sigma;
   bases.p[B_ARENA_L] = const_cast<double*>(plan->arena_l);
   bases.p[B_ARENA_R] = const_cast<double*>(plan->arena_r);
@@ -690,13 +811,13 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
       cudaEventRecord(ch.ev[1], stream);
       cudaEventRecord(ch.ev[2], stream);
     }
-    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 2 * c, stream);
+    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 2 * c, stream, true);
     if (rc) return rc;
     if (plan->timing) {
       cudaEventRecord(ch.ev[3], stream);
       cudaEventRecord(ch.ev[4], stream);
     }
-    rc = launch_engine(false, false, ch.p2, bases, plan->counters + 2 * c + 1, stream);
+    rc = launch_engine(false, false, ch.p2, bases, plan->counters + 2 * c + 1, stream, true);
     if (rc) return rc;
     if (plan->timing) {
       cudaEventRecord(ch.ev[5], stream);
@@ -759,6 +880,10 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
       if (e) cudaEventDestroy(e);
   }
   if (plan->workspace) cudaFree(plan->workspace);
+  if (plan->arena_l) cudaFree(plan->arena_l);
+  if (plan->arena_r) cudaFree(plan->arena_r);
+  if (plan->psi_pad) cudaFree(plan->psi_pad);
+  plan->psi_copy.release();
   if (plan->counters) cudaFree(plan->counters);
   delete plan;
   return SDMRG_OK;

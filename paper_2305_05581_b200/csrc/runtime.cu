@@ -32,9 +32,11 @@ static int grid_for() {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(seg_gemm_kernel<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem_bytes<TA, TB>());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, seg_gemm_kernel<TA, TB>, THREADS,
+    cudaFuncSetAttribute(seg_gemm_kernel<TA, TB, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<TA, TB>());
+    cudaFuncSetAttribute(seg_gemm_kernel<TA, TB, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<TA, TB>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, seg_gemm_kernel<TA, TB, true>, THREADS,
                                                   smem_bytes<TA, TB>());
     grid = sms * std::max(per, 1);
   }
@@ -158,19 +160,24 @@ int GemmBatch::upload(DeviceBatch* out, cudaStream_t stream) const {
 }
 
 template <bool TA, bool TB>
-static void launch_t(const DeviceBatch& b, const Bases& bases, int* counter, cudaStream_t stream) {
+static void launch_t(bool bulk, const DeviceBatch& b, const Bases& bases, int* counter,
+                     cudaStream_t stream) {
   const int grid = std::min<int64_t>(grid_for<TA, TB>(), std::max<int64_t>(b.ntiles, 1));
-  seg_gemm_kernel<TA, TB><<<grid, THREADS, smem_bytes<TA, TB>(), stream>>>(
-      b.tiles, static_cast<int>(b.ntiles), b.segs, counter, bases);
+  if (bulk)
+    seg_gemm_kernel<TA, TB, true><<<grid, THREADS, smem_bytes<TA, TB>(), stream>>>(
+        b.tiles, static_cast<int>(b.ntiles), b.segs, counter, bases);
+  else
+    seg_gemm_kernel<TA, TB, false><<<grid, THREADS, smem_bytes<TA, TB>(), stream>>>(
+        b.tiles, static_cast<int>(b.ntiles), b.segs, counter, bases);
 }
 
 int launch_engine(bool ta, bool tb, const DeviceBatch& b, const Bases& bases, int* counter,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, bool bulk) {
   if (b.ntiles == 0) return SDMRG_OK;
-  if (!ta && !tb) launch_t<false, false>(b, bases, counter, stream);
-  else if (!ta && tb) launch_t<false, true>(b, bases, counter, stream);
-  else if (ta && !tb) launch_t<true, false>(b, bases, counter, stream);
-  else launch_t<true, true>(b, bases, counter, stream);
+  if (!ta && !tb) launch_t<false, false>(bulk, b, bases, counter, stream);
+  else if (!ta && tb) launch_t<false, true>(bulk, b, bases, counter, stream);
+  else if (ta && !tb) launch_t<true, false>(bulk, b, bases, counter, stream);
+  else launch_t<true, true>(bulk, b, bases, counter, stream);
   count_launch();
   return cuda_check(cudaGetLastError(), "seg_gemm_kernel launch");
 }

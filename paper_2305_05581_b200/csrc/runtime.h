@@ -44,7 +44,9 @@ struct GemmBatch {
 
 // Launch the engine over an uploaded batch.  counter must point at one
 // zeroed device int (reset by the caller or by this function when reset=1).
+// bulk: every operand row 16-byte aligned, even leading dimensions, zero
+// pads (engine.cuh BULK) — the H_eff plan's padded layouts only.
 int launch_engine(bool ta, bool tb, const DeviceBatch& b, const Bases& bases, int* counter,
-                  cudaStream_t stream);
+                  cudaStream_t stream, bool bulk = false);
 
 }  // namespace sdmrg
