@@ -17,6 +17,7 @@
  * sdmrg_plan_build                blocks.py:503 build_plan (task generation:
  *                                 operator-table rows x ψ sectors -> work list)
  * sdmrg_plan_groups               blocks.py:563 the per-(ψ key, out key) groups
+ * sdmrg_plan_shard                (multi-GPU) ψ-sector ownership of a rank
  * sdmrg_plan_apply                dmrg.py:107  apply_plan (out += H_eff ψ)
  * sdmrg_dot / sdmrg_nrm2 /
  * sdmrg_gemv_t / sdmrg_gemv_n /
@@ -140,8 +141,8 @@ typedef struct sdmrg_plan_desc {
   const double* site1_val;
   const int32_t* site2_dst;
   const double* site2_val;
-  const double* arena_l;           /* device                                  */
-  const double* arena_r;           /* device                                  */
+  const double* arena_l;           /* device; repacked into plan-owned padded */
+  const double* arena_r;           /* memory at build (may be freed after)    */
   int64_t workspace_doubles;       /* budget for the T = A R^T staging (0 = auto) */
   int rank;
   int world;
@@ -181,6 +182,9 @@ int sdmrg_plan_layout(const sdmrg_plan* plan, int32_t* keys, int64_t* offsets);
 int sdmrg_plan_groups(const sdmrg_plan* plan, int32_t* group_psi,
                       int32_t* group_out, int64_t* group_begin,
                       int64_t* member_row, double* member_scale);
+/* Shard ownership: mine[i] = 1 when ψ key i is this rank's input sector
+ * (psi_keys entries).  Every key belongs to exactly one rank of `world`.    */
+int sdmrg_plan_shard(const sdmrg_plan* plan, int32_t* mine);
 /* sigma (+)= H_eff psi over this rank's shard; device vectors of psi_size. */
 int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma,
                      int accumulate, void* stream);

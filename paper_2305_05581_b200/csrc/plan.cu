@@ -142,6 +142,7 @@ struct sdmrg_plan {
   double* arena_r = nullptr;
   double* psi_pad = nullptr;       // padded ψ, refilled by every apply
   std::vector<int64_t> poffs;      // padded ψ block offsets (psi_keys + 1)
+  std::vector<char> mine;          // ψ keys of this rank's shard
   PadList psi_copy;                // ψ -> psi_pad block list (device)
   sdmrg_plan_stats stats{};
   int timing = 0;
@@ -432,6 +433,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       mine[idx] = (best == d->rank);
     }
   }
+
+  plan->mine = mine;
 
   // ---- execution schedule: chunks of ψ keys bounded by the workspace
   // (distinct non-identity T blocks + pre-summed left operators per key)
@@ -760,6 +763,12 @@ int sdmrg_plan_layout(const sdmrg_plan* plan, int32_t* keys, int64_t* offsets) {
   if (!plan) return fail(SDMRG_EINVAL, "plan_layout: null plan");
   if (keys) std::memcpy(keys, plan->keys.data(), plan->keys.size() * sizeof(int32_t));
   if (offsets) std::memcpy(offsets, plan->offs.data(), plan->offs.size() * sizeof(int64_t));
+  return SDMRG_OK;
+}
+
+int sdmrg_plan_shard(const sdmrg_plan* plan, int32_t* mine) {
+  if (!plan || !mine) return fail(SDMRG_EINVAL, "plan_shard: null argument");
+  for (size_t i = 0; i < plan->mine.size(); ++i) mine[i] = plan->mine[i] ? 1 : 0;
   return SDMRG_OK;
 }
 

@@ -151,6 +151,12 @@ class DevicePlan:
             P(mr, ctypes.c_int64), P(ms, ctypes.c_double)))
         return PlanGroups(gp, go, gb, mr, ms)
 
+    def shard(self):
+        """Boolean mask over ψ keys: the input sectors this rank applies."""
+        mine = np.zeros(self.stats["psi_keys"], np.int32)
+        _lib.check(_lib.load().sdmrg_plan_shard(self._h, _lib.as_p(mine, ctypes.c_int32)))
+        return mine.astype(bool)
+
     def empty_vector(self):
         return torch.empty(self.psi_size, dtype=torch.float64, device=self.device)
 
