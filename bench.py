@@ -125,6 +125,19 @@ def dgemm_peak(torch):
     return 2 * n ** 3 / (best * 1e-3) / 1e12
 
 
+def ncu_traffic(kernel, args):
+    """DRAM bytes per launch of ``kernel`` from the committed ncu capture
+    (profiles/traffic.json, dram__bytes_read.sum + dram__bytes_write.sum of
+    one --set full launch at the default workload), else None."""
+    if (args.L, args.D) != (30, 2048):
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
 def hbm_peak():
     """HBM roofline denominator: MEASURED_PEAKS.json, else the recipe fallback."""
     try:
@@ -349,7 +362,7 @@ def run_b200(args):
         achieved = phase_flops[dom] / (phase_ms[dom] * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s"}
     roof.update({"frac": roof["achieved"] / roof["peak"] if roof["peak"] else None,
-                 "traffic": None, "kernel": names[dom],
+                 "traffic": ncu_traffic(names[dom], args), "kernel": names[dom],
                  "peak_source": ("measured live: cuBLAS DGEMM 8192^3 burst (torch.matmul f64)"
                                  if dom in (1, 2) else "MEASURED_PEAKS.json hbm_gbs"),
                  "phase_ms": phase_ms, "phase_exec_flops": phase_flops,
