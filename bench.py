@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scale-d", default="4096",
+                    help="comma list of extra bond dimensions timed at N=1 (north-star scale "
+                         "points, reported under 'scale_points'); empty to skip")
     return ap.parse_args()
 
 
@@ -187,6 +190,43 @@ def cpu_sample(pi, plan_groups, keys_order, arena_l, arena_r, budget_s, psi):
         if t_total >= budget_s:
             break
     return done_flops / t_total / 1e12, t_total, done_flops, done_groups
+
+
+def scale_point(n_orb, d, seed, peak, applies=3):
+    """One H_eff·ψ at a larger bond dimension (north star: D >= 4096): device
+    ms per apply, reference TFLOP/s, engine TFLOP/s and its fraction of the
+    DGEMM peak.  Inputs resident, 1 warm-up, best of ``applies``."""
+    import torch
+    from paper_2305_05581_b200.plan import DevicePlan
+    from paper_2305_05581_b200.workload import fill_arenas_device, synthetic_plan_input
+    pi = synthetic_plan_input(n_orb, d, seed=seed)
+    al, ar = fill_arenas_device(pi, seed=seed)
+    plan = DevicePlan(pi, arena_l=al, arena_r=ar)
+    del al, ar
+    torch.cuda.empty_cache()
+    st = plan.stats
+    psi = torch.randn(plan.psi_size, dtype=torch.float64, device="cuda")
+    out = plan.empty_vector()
+    plan.apply(psi, out)
+    best = 1e30
+    for _ in range(applies):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        plan.apply(psi, out)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    res = {"workload": f"CAS({n_orb},{n_orb}) synthetic, U(1)xU(1), D={d}, one H_eff·psi",
+           "D": d, "ms_per_step": best, "ref_tflops": st["ref_flops"] / (best * 1e-3) / 1e12,
+           "exec_tflops": st["exec_flops"] / (best * 1e-3) / 1e12,
+           "exec_frac_of_dgemm": (st["exec_flops"] / (best * 1e-3) / 1e12) / peak if peak else None,
+           "chunks": st["chunks"], "psi_size": st["psi_size"]}
+    plan.close()
+    del plan, psi, out
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_reference(args):
@@ -350,6 +390,14 @@ def run_b200(args):
                          f"the step's FLOPs, {secs:.1f}s) through oracle.heff.apply_groups "
                          f"(reference sbmm4s per group, NumPy BLAS)"}
 
+    scale = []
+    if world == 1 and args.scale_d:
+        del plan, psi, sigma
+        al = ar = None
+        torch.cuda.empty_cache()
+        for d in [int(x) for x in args.scale_d.split(",") if x.strip()]:
+            scale.append(scale_point(args.L, d, args.seed, peak))
+
     value = st["ref_flops"] / (ms * 1e-3) / 1e12
     dom = int(np.argmax(phase_ms))
     names = ["combine_kernel (phase 0: Lsum = sum s L)", "seg_gemm_kernel<0,1> (phase 1: T = A R^T)",
@@ -376,7 +424,7 @@ def run_b200(args):
                    "parallelism": f"psi-sector shards x{world} + NCCL allreduce(sigma)",
                    "l2": "inputs larger than L2 (operator arenas 2x%.1f GB)" % (
                        pi.meta["arena_size_l"] * 8 / 1e9),
-                   "psi_size": plan.psi_size, "psi_keys": st["psi_keys"],
+                   "psi_size": st["psi_size"], "psi_keys": st["psi_keys"],
                    "groups": st["groups"], "members": st["members"],
                    "ref_flops_per_step": st["ref_flops"],
                    "exec_flops_per_step_rank0": st["exec_flops"],
@@ -385,6 +433,7 @@ def run_b200(args):
         "exec_tflops": st["exec_flops"] * world / (ms * 1e-3) / 1e12,
         "roofline": roof,
         "cpu_baseline": cpu,
+        "scale_points": scale,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,

@@ -198,14 +198,26 @@ __global__ void scale_cm_kernel(int m, int n, double s, double* c, int ldc) {
 }
 
 // One-shot launch of a host-built batch (uploads, launches, frees).
+// Every operand of the batch 16-byte aligned with even leading dimensions:
+// the engine may use 16-byte cp.async (engine.cuh ALIGNED).
+static bool batch_aligned(const GemmBatch& gb, const Bases& bases) {
+  for (const Seg& sg : gb.segs) {
+    const uint64_t a = reinterpret_cast<uint64_t>(bases.p[sg.a >> kHandleShift] + (sg.a & kHandleMask));
+    const uint64_t b = reinterpret_cast<uint64_t>(bases.p[sg.b >> kHandleShift] + (sg.b & kHandleMask));
+    if ((a & 15) || (b & 15) || (sg.lda & 1) || (sg.ldb & 1)) return false;
+  }
+  return true;
+}
+
 static int run_batch(GemmBatch& gb, bool ta, bool tb, const Bases& bases, cudaStream_t stream) {
   gb.finalize_tiles();
+  const bool aligned = batch_aligned(gb, bases);
   DeviceBatch db;
   int rc = gb.upload(&db, stream);
   int* counter = nullptr;
   if (!rc) rc = cuda_check(cudaMalloc(&counter, sizeof(int)), "cudaMalloc counter");
   if (!rc) rc = cuda_check(cudaMemsetAsync(counter, 0, sizeof(int), stream), "memset counter");
-  if (!rc) rc = launch_engine(ta, tb, db, bases, counter, stream);
+  if (!rc) rc = launch_engine(ta, tb, db, bases, counter, stream, aligned);
   if (!rc) rc = cuda_check(cudaStreamSynchronize(stream), "batch sync");
   if (counter) cudaFree(counter);
   db.release();
