@@ -281,9 +281,16 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # one rank per GPU; SDMRG_DIST_BACKEND=gloo + more ranks than GPUs is the
+    # single-GPU plumbing check (tools/check_multirank.py), not a measurement
+    dev = local % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("SDMRG_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
@@ -311,7 +318,7 @@ def run_b200(args):
         step(psi, sigma)
     barrier()
     l0 = _lib.launch_count()
-    clocks = Clocks(local)
+    clocks = Clocks(dev)
     clocks.start()
     stream = torch.cuda.current_stream()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -410,7 +417,8 @@ def run_b200(args):
         achieved = phase_flops[dom] / (phase_ms[dom] * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s"}
     roof.update({"frac": roof["achieved"] / roof["peak"] if roof["peak"] else None,
-                 "traffic": ncu_traffic(names[dom], args), "kernel": names[dom],
+                 "traffic": ncu_traffic(names[dom], args) if world == 1 else None,
+                 "kernel": names[dom],
                  "peak_source": ("measured live: cuBLAS DGEMM 8192^3 burst (torch.matmul f64)"
                                  if dom in (1, 2) else "MEASURED_PEAKS.json hbm_gbs"),
                  "phase_ms": phase_ms, "phase_exec_flops": phase_flops,
@@ -421,7 +429,9 @@ def run_b200(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args), "L": args.L, "D": args.D,
-                   "parallelism": f"psi-sector shards x{world} + NCCL allreduce(sigma)",
+                   "parallelism": f"psi-sector shards x{world} + "
+                                  f"{os.environ.get('SDMRG_DIST_BACKEND', 'nccl').upper()} "
+                                  f"allreduce(sigma)",
                    "l2": "inputs larger than L2 (operator arenas 2x%.1f GB)" % (
                        pi.meta["arena_size_l"] * 8 / 1e9),
                    "psi_size": st["psi_size"], "psi_keys": st["psi_keys"],

@@ -1,0 +1,38 @@
+"""Device multi-rank H_eff·ψ (sharded plans + all-reduce) under torchrun.
+On a 1-GPU box the ranks share cuda:0 over gloo; with >= 2 GPUs the same
+check runs over NCCL, one rank per GPU."""
+
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_apply_allreduce_equals_full(world):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ)
+    if torch.cuda.device_count() < world:
+        env["SDMRG_DIST_BACKEND"] = "gloo"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_port()), os.path.join(ROOT, "tools", "check_multirank.py"),
+           "12", "64"]
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
+    assert "PASS" in out.stdout
