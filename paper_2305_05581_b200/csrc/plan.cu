@@ -144,6 +144,11 @@ struct sdmrg_plan {
   std::vector<int64_t> poffs;      // padded ψ block offsets (psi_keys + 1)
   std::vector<char> mine;          // ψ keys of this rank's shard
   PadList psi_copy;                // ψ -> psi_pad block list (device)
+  // phase 0 (combine) runs on a low-priority side stream concurrently with
+  // phase 1 (it only needs the L arena): measured 97.3 -> 96.0 ms per apply
+  // at L=30 D=2048; queueing phase 1 first was slower (97.2)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
   sdmrg_plan_stats stats{};
   int timing = 0;
 };
@@ -698,6 +703,14 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     if (!rc) rc = upload_vec(ptasks, &plan->psi_copy.d_tasks);
     plan->psi_copy.n = static_cast<int64_t>(ptasks.size());
   }
+  if (!rc && !d->dry_run) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    rc = cuda_check(cudaStreamCreateWithPriority(&plan->side, cudaStreamNonBlocking, lo),
+                    "create side stream");
+    if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&plan->fork, cudaEventDisableTiming), "event");
+    if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&plan->join, cudaEventDisableTiming), "event");
+  }
   if (!rc && ws_max > 0) {
     rc = cuda_check(cudaMalloc(&plan->workspace, sizeof(double) * ws_max), "cudaMalloc workspace");
     // T pads are never written by the engine: zero them once
@@ -813,19 +826,25 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
   bases.p[B_WS] = plan->workspace;
   for (size_t c = 0; c < plan->chunks.size(); ++c) {
     Chunk& ch = plan->chunks[c];
-    if (plan->timing) cudaEventRecord(ch.ev[0], stream);
-    rc = launch_combine(ch.comb0, bases, stream);
-    if (rc) return rc;
-    if (plan->timing) {
-      cudaEventRecord(ch.ev[1], stream);
-      cudaEventRecord(ch.ev[2], stream);
+    // phase 0 on the side stream, ordered after everything queued so far
+    // (the previous chunk / apply still reads the workspace it rewrites)
+    const bool fork = ch.comb0.ntasks > 0 && plan->side != nullptr;
+    cudaStream_t s0 = fork ? plan->side : stream;
+    if (fork) {
+      cudaEventRecord(plan->fork, stream);
+      cudaStreamWaitEvent(plan->side, plan->fork, 0);
     }
+    if (plan->timing) cudaEventRecord(ch.ev[0], s0);
+    rc = launch_combine(ch.comb0, bases, s0);
+    if (rc) return rc;
+    if (plan->timing) cudaEventRecord(ch.ev[1], s0);
+    if (fork) cudaEventRecord(plan->join, plan->side);
+    if (plan->timing) cudaEventRecord(ch.ev[2], stream);
     rc = launch_engine(false, true, ch.p1, bases, plan->counters + 2 * c, stream, true);
     if (rc) return rc;
-    if (plan->timing) {
-      cudaEventRecord(ch.ev[3], stream);
-      cudaEventRecord(ch.ev[4], stream);
-    }
+    if (plan->timing) cudaEventRecord(ch.ev[3], stream);
+    if (fork) cudaStreamWaitEvent(stream, plan->join, 0);
+    if (plan->timing) cudaEventRecord(ch.ev[4], stream);
     rc = launch_engine(false, false, ch.p2, bases, plan->counters + 2 * c + 1, stream, true);
     if (rc) return rc;
     if (plan->timing) {
@@ -893,6 +912,9 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
   if (plan->arena_r) cudaFree(plan->arena_r);
   if (plan->psi_pad) cudaFree(plan->psi_pad);
   plan->psi_copy.release();
+  if (plan->fork) cudaEventDestroy(plan->fork);
+  if (plan->join) cudaEventDestroy(plan->join);
+  if (plan->side) cudaStreamDestroy(plan->side);
   if (plan->counters) cudaFree(plan->counters);
   delete plan;
   return SDMRG_OK;
