@@ -104,10 +104,18 @@ struct Seg {         // 40 B
 #ifndef SDMRG_STAGES
 #define SDMRG_STAGES 4
 #endif
-#ifndef SDMRG_MINB
-#define SDMRG_MINB 3
+#ifndef SDMRG_TILE
+#define SDMRG_TILE 64
 #endif
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = SDMRG_STAGES;
+#ifndef SDMRG_DB
+#define SDMRG_DB 0
+#endif
+#ifndef SDMRG_MINB
+#define SDMRG_MINB (SDMRG_TILE > 64 ? 2 : 3)
+#endif
+constexpr int BM = SDMRG_TILE, BN = SDMRG_TILE, BK = 16, STAGES = SDMRG_STAGES;
+constexpr int MAXB = BM / 16;                    // 8x8 blocks per warp and dimension
+static_assert(BM == 64 || BM == 96, "tile edge 64 or 96");
 constexpr int CONSUMERS = 4, WGRID_R = 2, WGRID_C = 2;
 constexpr int THREADS = 32 * (CONSUMERS + 1);
 constexpr int KC_LD = BK + 2;                    // K-contiguous row stride (144 B)
@@ -228,6 +236,43 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
     const double scale = m.scale;
     const uint32_t a0 = ring.smem + stage * STAGE_B + a_off;
     const uint32_t b0 = ring.smem + stage * STAGE_B + b_off;
+#if SDMRG_DB
+    if (MB > 0 && NB > 0 && nks > 0) {
+      // fragments of k4 step ks+1 loaded (and scaled) around the DMMAs of ks
+      const bool scaled = scale != 1.0;
+      double af[2][MB > 0 ? MB : 1], bf[2][NB > 0 ? NB : 1];
+      auto load = [&](int ks, int buf) {
+#pragma unroll
+        for (int i = 0; i < MB; ++i) af[buf][i] = lds64(a0 + ks * A_KS + i * A_I);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) bf[buf][j] = lds64(b0 + ks * B_KS + j * B_J);
+      };
+      auto rescale = [&](int buf) {
+        if (NB <= MB) {
+#pragma unroll
+          for (int j = 0; j < NB; ++j) bf[buf][j] *= scale;
+        } else {
+#pragma unroll
+          for (int i = 0; i < MB; ++i) af[buf][i] *= scale;
+        }
+      };
+      load(0, 0);
+      if (scaled) rescale(0);
+#pragma unroll
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        if (ks < nks) {
+          const int cur = ks & 1, nxt = cur ^ 1;
+          const bool more = ks + 1 < BK / 4 && ks + 1 < nks;
+          if (more) load(ks + 1, nxt);
+#pragma unroll
+          for (int i = 0; i < MB; ++i)
+#pragma unroll
+            for (int j = 0; j < NB; ++j) dmma(acc[i][j], af[cur][i], bf[cur][j]);
+          if (more && scaled) rescale(nxt);
+        }
+      }
+    }
+#else
     if (MB > 0 && NB > 0) {
 #ifdef SDMRG_EXP_NOSCALE
       const bool scaled = false;
@@ -260,6 +305,7 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
         }
       }
     }
+#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(ring.empty0 + 8 * stage);
     if (++stage == STAGES) {
@@ -302,6 +348,13 @@ __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring&
                                                  double* c, int ldc, int beta, int row_lim,
                                                  int col_lim, int lane) {
   switch (mblk * 8 + nblk) {
+#if SDMRG_TILE > 64
+    SDMRG_TILE_CASE(6, 6) SDMRG_TILE_CASE(6, 5) SDMRG_TILE_CASE(5, 6) SDMRG_TILE_CASE(5, 5)
+    SDMRG_TILE_CASE(6, 4) SDMRG_TILE_CASE(6, 3) SDMRG_TILE_CASE(6, 2) SDMRG_TILE_CASE(6, 1)
+    SDMRG_TILE_CASE(5, 4) SDMRG_TILE_CASE(5, 3) SDMRG_TILE_CASE(5, 2) SDMRG_TILE_CASE(5, 1)
+    SDMRG_TILE_CASE(4, 6) SDMRG_TILE_CASE(4, 5) SDMRG_TILE_CASE(3, 6) SDMRG_TILE_CASE(3, 5)
+    SDMRG_TILE_CASE(2, 6) SDMRG_TILE_CASE(2, 5) SDMRG_TILE_CASE(1, 6) SDMRG_TILE_CASE(1, 5)
+#endif
     SDMRG_TILE_CASE(4, 4) SDMRG_TILE_CASE(4, 3) SDMRG_TILE_CASE(4, 2) SDMRG_TILE_CASE(4, 1)
     SDMRG_TILE_CASE(3, 4) SDMRG_TILE_CASE(3, 3) SDMRG_TILE_CASE(3, 2) SDMRG_TILE_CASE(3, 1)
     SDMRG_TILE_CASE(2, 4) SDMRG_TILE_CASE(2, 3) SDMRG_TILE_CASE(2, 2) SDMRG_TILE_CASE(2, 1)
@@ -340,7 +393,7 @@ __device__ __forceinline__ void load_operand_async(uint32_t sbase, const double*
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < BM / 32; ++j) {
       const int c = lane + 32 * j;
       if (c < extent) {
         const double* p = src + c;
@@ -363,7 +416,7 @@ __device__ __forceinline__ void load_operand_async(uint32_t sbase, const double*
 // aligned in global and shared memory):
 //   K-contiguous: lane -> k pair kp = lane & 7 (k = 2kp, 2kp+1), rows
 //     (lane >> 3) + 4i, i < 16;
-//   M/N-contiguous: lane -> column pair (2 lane, 2 lane + 1), k = 0..15.
+//   M/N-contiguous: lane -> column pairs (2 lane + 64 j, +1), k = 0..15.
 // A pair straddling the k tail copies its first element and zero-fills the
 // second (src-size 8); pairs past the tail are zero-filled (src-size 0).
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const double* gmem, int src_bytes) {
@@ -392,17 +445,21 @@ __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const doubl
       for (int i = 0; i < nrow; ++i) cp_async16(s0 + i * (4 * KC_LD * 8), q + i * step, bytes);
     }
   } else {
-    const int c = 2 * lane;
-    if (c < extent) {
-      const double* p = src + c;
-      const uint32_t s0 = sbase + c * 8;
-      if (krem >= BK) {
 #pragma unroll
-        for (int k = 0; k < BK; ++k) cp_async16_full(s0 + k * (NC_LD * 8), p + (int64_t)k * ld);
-      } else {
+    for (int j = 0; j < (BM + 63) / 64; ++j) {
+      const int c = 2 * lane + 64 * j;
+      if (c < extent) {
+        const double* p = src + c;
+        const uint32_t s0 = sbase + c * 8;
+        if (krem >= BK) {
 #pragma unroll
-        for (int k = 0; k < BK; ++k)
-          cp_async16(s0 + k * (NC_LD * 8), k < krem ? p + (int64_t)k * ld : src, k < krem ? 16 : 0);
+          for (int k = 0; k < BK; ++k) cp_async16_full(s0 + k * (NC_LD * 8), p + (int64_t)k * ld);
+        } else {
+#pragma unroll
+          for (int k = 0; k < BK; ++k)
+            cp_async16(s0 + k * (NC_LD * 8), k < krem ? p + (int64_t)k * ld : src,
+                       k < krem ? 16 : 0);
+        }
       }
     }
   }
@@ -560,8 +617,13 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
 // BULK ("aligned"): every operand block 16-byte aligned with even leading
 // dimensions (the H_eff plan's padded layouts) -> 16-byte cp.async; the
 // launcher selects it per batch.
+#if SDMRG_TILE > 64
+#define SDMRG_KERNEL_BOUNDS __maxnreg__(200)
+#else
+#define SDMRG_KERNEL_BOUNDS __launch_bounds__(THREADS, SDMRG_MINB)
+#endif
 template <bool TA, bool TB, bool BULK>
-__global__ void __launch_bounds__(THREADS, SDMRG_MINB)
+__global__ void SDMRG_KERNEL_BOUNDS
 seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __restrict__ segs,
                 int* __restrict__ counter, Bases bases) {
   extern __shared__ __align__(128) double smem[];
