@@ -406,7 +406,9 @@ def run_b200(args):
             scale.append(scale_point(args.L, d, args.seed, peak))
 
     value = st["ref_flops"] / (ms * 1e-3) / 1e12
-    dom = int(np.argmax(phase_ms))
+    dom = 1 if phase_ms[1] >= phase_ms[2] else 2   # the tensor-bound engine phases
+    if max(phase_ms[0], phase_ms[3]) > phase_ms[dom]:
+        dom = 0 if phase_ms[0] >= phase_ms[3] else 3
     names = ["combine_kernel (phase 0: Lsum = sum s L)", "seg_gemm_kernel<0,1> (phase 1: T = A R^T)",
              "seg_gemm_kernel<0,0> (phase 2: sigma += Lsum T)",
              "combine_kernel (phase 3: split-K partials into sigma)"]

@@ -21,6 +21,7 @@
 //      shared inner dimension (no reduction pass, no atomics).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -144,9 +145,10 @@ struct sdmrg_plan {
   std::vector<int64_t> poffs;      // padded ψ block offsets (psi_keys + 1)
   std::vector<char> mine;          // ψ keys of this rank's shard
   PadList psi_copy;                // ψ -> psi_pad block list (device)
-  // phase 0 (combine) runs on a low-priority side stream concurrently with
-  // phase 1 (it only needs the L arena): measured 97.3 -> 96.0 ms per apply
-  // at L=30 D=2048; queueing phase 1 first was slower (97.2)
+  // optional (SDMRG_SIDE_STREAM=1): phase 0 (combine) on a low-priority side
+  // stream concurrently with phase 1 (it only needs the L arena).  Measured
+  // no gain at L=30 D=2048 (99.0 vs 99.4 ms, same box), and it blurs the
+  // per-phase timing, so phases run in order on the caller's stream.
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
   sdmrg_plan_stats stats{};
@@ -703,7 +705,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     if (!rc) rc = upload_vec(ptasks, &plan->psi_copy.d_tasks);
     plan->psi_copy.n = static_cast<int64_t>(ptasks.size());
   }
-  if (!rc && !d->dry_run) {
+  if (!rc && !d->dry_run && getenv("SDMRG_SIDE_STREAM")) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     rc = cuda_check(cudaStreamCreateWithPriority(&plan->side, cudaStreamNonBlocking, lo),
