@@ -347,6 +347,24 @@ def run_b200(args):
     phase_ms = [float(np.mean([p[0][k] for p in ph])) for k in range(4)]
     phase_flops, phase_bytes = ph[0][1], ph[0][2]
 
+    # Krylov step cost (north star item 4): 10 device Lanczos iterations
+    # (dmrg.py:43 loop: apply + full CGS2 reorthogonalisation + 2 scalars to
+    # the host) on this H_eff — tolerance 0 so none converges early; 11
+    # applies (10 + the final residual) of which the vector algebra is the rest
+    krylov = None
+    if world == 1:
+        from paper_2305_05581_b200.lanczos import lanczos_ground
+        buf = plan.empty_vector()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = lanczos_ground(lambda v: plan.apply(v, buf), psi, tol=0.0, max_iter=10)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        krylov = {"iterations": res.iterations, "applies": res.iterations + 1,
+                  "wall_ms": wall, "ms_per_iteration": wall / res.iterations,
+                  "non_apply_ms_per_iteration": (wall - (res.iterations + 1) * ms) /
+                  res.iterations}
+
     # e2e: host ψ in (pinned), σ back every step, through the public API
     e2e = None
     if not args.no_e2e:
@@ -447,6 +465,7 @@ def run_b200(args):
         "cpu_baseline": cpu,
         "scale_points": scale,
         "e2e": e2e,
+        "krylov": krylov,
         "gpu_launches": int(launches),
         "clocks": clk,
     }

@@ -292,3 +292,22 @@ def test_cuda_gemm_backend_contract_with_interleaved_views():
     c0 = c.copy()
     be.add_inplace(c, np.ones((2, 2)), alpha=2.0)
     assert rel_err(c, c0 + 2.0) < 1e-15
+
+
+def test_plan_apply_edge_cases(golden):
+    """Empty table: σ = 0 (accumulate leaves σ unchanged); one row: matches
+    the oracle; zero-coefficient table: σ = 0."""
+    from paper_2305_05581_b200.plan import DevicePlan
+    from test_oracle_golden import _rows_subset
+    name, pi = golden
+    psi = torch.from_numpy(pi.meta["psi"]).cuda()
+    empty = _rows_subset(pi, np.zeros(pi.nrows, bool))
+    p = DevicePlan(empty)
+    assert torch.count_nonzero(p.apply(psi)) == 0
+    acc = torch.full_like(psi, 3.0)
+    p.apply(psi, acc, accumulate=True)
+    assert torch.all(acc == 3.0)
+    one = _rows_subset(pi, np.arange(pi.nrows) == min(1, pi.nrows - 1))
+    ref = heff.apply_heff(one, pi.meta["psi"])
+    got = DevicePlan(one).apply(psi).cpu().numpy()
+    assert rel_err(got, ref) <= 1e-12

@@ -161,3 +161,31 @@ def test_oracle_rotation_matches_reference(golden):
         ref = m["renorm_hrot_data"][pos:pos + n].reshape(kdims[q], kdims[q])
         pos += n
         assert np.max(np.abs(rot[(q, q)] - ref)) <= 1e-12 * (1 + np.max(np.abs(ref)))
+
+
+def _rows_subset(pi, sel):
+    """The same partition with only table rows ``sel`` (edge cases)."""
+    import copy
+    q = copy.copy(pi)
+    for name in ("lop", "rop", "alpha", "e_l", "site1_dst", "site1_val", "site2_dst",
+                 "site2_val", "row_map"):
+        setattr(q, name, getattr(pi, name)[sel])
+    q.meta = dict(pi.meta)
+    return q.normalized()
+
+
+def test_native_task_generation_edge_cases(golden):
+    """No rows -> no members and zero FLOPs; a single row -> the oracle's
+    grouping of that row; zero coefficients are dropped (blocks.py:561)."""
+    from paper_2305_05581_b200.plan import DevicePlan
+    _name, pi = golden
+    empty = _rows_subset(pi, np.zeros(pi.nrows, bool))
+    st = DevicePlan(empty, dry_run=True).stats
+    assert st["members"] == 0 and st["ref_flops"] == 0 and st["groups"] == 0
+    assert st["psi_size"] == pi.meta["psi"].size
+    one = _rows_subset(pi, np.arange(pi.nrows) == 1)
+    plan = DevicePlan(one, dry_run=True, keep_groups=True)
+    assert plan.stats["members"] == sum(len(m) for _i, _o, m in heff.build_groups(one))
+    zero = _rows_subset(pi, np.ones(pi.nrows, bool))
+    zero.alpha = np.zeros_like(zero.alpha)
+    assert DevicePlan(zero.normalized(), dry_run=True).stats["members"] == 0
