@@ -6,6 +6,9 @@
 // bitwise reproducible run to run and identical on every rank that holds the
 // same vectors (replicated Krylov space across GPUs).
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "../../include/sdmrg_b200.h"
 #include "runtime.h"
@@ -90,19 +93,43 @@ static int grid_for_n(int64_t n) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
 }
 
+// Reduction partials: one grow-only device buffer per (device, stream),
+// reused by every call on that stream (stream order makes reuse safe).  A
+// per-call cudaMallocAsync measured ~90 ms per Lanczos reorthogonalisation
+// pass once the plan's large allocations had pushed the async pool to
+// return memory at every host synchronisation.
+static int partials_for(cudaStream_t stream, size_t doubles, double** out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<double*, size_t>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = cache[{dev, stream}];
+  if (slot.second < doubles) {
+    if (slot.first) {
+      cudaStreamSynchronize(stream);
+      cudaFree(slot.first);
+      slot = {nullptr, 0};
+    }
+    const size_t want = std::max<size_t>(doubles, 64 * kRedBlocks);
+    int rc = cuda_check(cudaMalloc(&slot.first, sizeof(double) * want), "cudaMalloc partials");
+    if (rc) return rc;
+    slot.second = want;
+  }
+  *out = slot.first;
+  return SDMRG_OK;
+}
+
 static int dots(int k, int64_t n, const double* v, int64_t ldv, const double* w, double* out,
                 int sqrt_out, cudaStream_t stream) {
   if (k <= 0) return SDMRG_OK;
   double* partial = nullptr;
-  int rc = cuda_check(cudaMallocAsync(&partial, sizeof(double) * (size_t)k * kRedBlocks, stream),
-                      "cudaMallocAsync partials");
+  int rc = partials_for(stream, (size_t)k * kRedBlocks, &partial);
   if (rc) return rc;
   dots_partial<<<dim3(kRedBlocks, k), kRedThreads, 0, stream>>>(n, v, ldv, w, partial);
   dots_final<<<(k + 7) / 8, 256, 0, stream>>>(k, kRedBlocks, partial, out, sqrt_out);
   count_launch(2);
-  rc = cuda_check(cudaGetLastError(), "dots launch");
-  cudaFreeAsync(partial, stream);
-  return rc;
+  return cuda_check(cudaGetLastError(), "dots launch");
 }
 
 }  // namespace sdmrg
