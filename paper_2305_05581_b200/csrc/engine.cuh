@@ -49,6 +49,7 @@
 //   M/N-contiguous operand tile [16][64+4]:                (k, r) -> k*68 + r
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace sdmrg {
@@ -279,31 +280,39 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
 #else
       const bool scaled = scale != 1.0;
 #endif
+      // the scale branch is warp-uniform per stage; two bodies keep ptxas
+      // from if-converting the DMULs into unscaled stages (phase 1 never
+      // scales, and a DMUL takes FP64-pipe slots from the DMMAs)
+      auto body = [&](auto scaled_t) {
+        constexpr bool SCALED = decltype(scaled_t)::value;
 #pragma unroll
-      for (int ks = 0; ks < BK / 4; ++ks) {
-        if (ks < nks) {
-          double af[MB > 0 ? MB : 1], bf[NB > 0 ? NB : 1];
+        for (int ks = 0; ks < BK / 4; ++ks) {
+          if (ks < nks) {
+            double af[MB > 0 ? MB : 1], bf[NB > 0 ? NB : 1];
 #pragma unroll
-          for (int i = 0; i < MB; ++i) af[i] = lds64(a0 + ks * A_KS + i * A_I);
+            for (int i = 0; i < MB; ++i) af[i] = lds64(a0 + ks * A_KS + i * A_I);
 #pragma unroll
-          for (int j = 0; j < NB; ++j) bf[j] = lds64(b0 + ks * B_KS + j * B_J);
-          if (scaled) {
-            if (NB <= MB) {
+            for (int j = 0; j < NB; ++j) bf[j] = lds64(b0 + ks * B_KS + j * B_J);
+            if (SCALED) {
+              if (NB <= MB) {
 #pragma unroll
-              for (int j = 0; j < NB; ++j) bf[j] *= scale;
-            } else {
+                for (int j = 0; j < NB; ++j) bf[j] *= scale;
+              } else {
 #pragma unroll
-              for (int i = 0; i < MB; ++i) af[i] *= scale;
+                for (int i = 0; i < MB; ++i) af[i] *= scale;
+              }
             }
-          }
 #ifndef SDMRG_EXP_NOMMA
 #pragma unroll
-          for (int i = 0; i < MB; ++i)
+            for (int i = 0; i < MB; ++i)
 #pragma unroll
-            for (int j = 0; j < NB; ++j) dmma(acc[i][j], af[i], bf[j]);
+              for (int j = 0; j < NB; ++j) dmma(acc[i][j], af[i], bf[j]);
 #endif
+          }
         }
-      }
+      };
+      if (scaled) body(std::true_type{});
+      else body(std::false_type{});
     }
 #endif
     __syncwarp();
@@ -528,21 +537,28 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
   };
   int stage = 0;
   uint32_t phase = 0;
-  int t = 0;
-  if (lane == 0) t = atomicAdd(counter, 1);
+  // Tile queue with two tiles of lookahead: the index of tile i+2 is claimed
+  // while tile i streams and its descriptor is loaded at the end of tile i, so
+  // neither the atomic nor the dependent descriptor load sits on the path
+  // between two tiles (consumers measured waiting at tile starts otherwise).
+  int t = 0, t1 = 0;
+  if (lane == 0) {
+    t = atomicAdd(counter, 1);
+    t1 = atomicAdd(counter, 1);
+  }
   t = __shfl_sync(0xffffffffu, t, 0);
-  TileRec cur{};
+  t1 = __shfl_sync(0xffffffffu, t1, 0);
+  TileRec cur{}, nrec{};
   Seg sn{};                       // prefetched next segment descriptor
   if (t < ntiles) {
     cur = tiles[t];
     if (cur.seg_begin < cur.seg_end) sn = segs[cur.seg_begin];
   }
+  if (t1 < ntiles) nrec = tiles[t1];
   while (t < ntiles) {
-    int next = 0;
-    if (lane == 0) next = atomicAdd(counter, 1);  // one tile of lookahead
-    next = __shfl_sync(0xffffffffu, next, 0);
-    TileRec nrec{};
-    if (next < ntiles) nrec = tiles[next];
+    int t2 = 0;
+    if (lane == 0) t2 = atomicAdd(counter, 1);  // resolved by the end of this tile
+    const int next = t1;
     double* cptr = sbases[cur.c >> kHandleShift] + (cur.c & kHandleMask) +
                    (int64_t)cur.row0 * cur.ldc + cur.col0;
     if (cur.seg_begin == cur.seg_end) {
@@ -606,8 +622,13 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
         }
       }
     }
+    t2 = __shfl_sync(0xffffffffu, t2, 0);
+    TileRec n2{};
+    if (t2 < ntiles) n2 = tiles[t2];
     t = next;
     cur = nrec;
+    nrec = n2;
+    t1 = t2;
   }
   mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
   meta_write(stage, 0, 1.0, kEnd, cur, nullptr);
