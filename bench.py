@@ -48,9 +48,10 @@ def parse():
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--scale-d", default="4096",
-                    help="comma list of extra bond dimensions timed at N=1 (north-star scale "
-                         "points, reported under 'scale_points'); empty to skip")
+    ap.add_argument("--scale", default="30:4096,50:4096",
+                    help="comma list of L:D workloads also timed at N=1 (north-star scale "
+                         "points: D >= 4096, the L=50 CAS table; reported under "
+                         "'scale_points'); empty to skip")
     return ap.parse_args()
 
 
@@ -416,12 +417,13 @@ def run_b200(args):
                          f"(reference sbmm4s per group, NumPy BLAS)"}
 
     scale = []
-    if world == 1 and args.scale_d:
+    if world == 1 and args.scale:
         del plan, psi, sigma
         al = ar = None
         torch.cuda.empty_cache()
-        for d in [int(x) for x in args.scale_d.split(",") if x.strip()]:
-            scale.append(scale_point(args.L, d, args.seed, peak))
+        for item in [x for x in args.scale.split(",") if x.strip()]:
+            n_orb, d = (int(v) for v in item.split(":"))
+            scale.append(scale_point(n_orb, d, args.seed, peak))
 
     value = st["ref_flops"] / (ms * 1e-3) / 1e12
     dom = 1 if phase_ms[1] >= phase_ms[2] else 2   # the tensor-bound engine phases

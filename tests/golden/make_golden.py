@@ -14,7 +14,7 @@ the reference's own model / factorize / block stores, then records:
   * a renormalization step: reference renormalize (dmrg.py:335) outputs —
     kept sector dims, truncation error, W, and the rotated H operator.
 
-Usage:  python tests/golden/make_golden.py
+Usage:  python tests/golden/make_golden.py [case ...]
 """
 
 import os
@@ -161,19 +161,22 @@ def record(name, model, p, left, right, target, seed=7):
           f"iters {lz.iterations} trunc {rr.truncation_error:.3e} -> {path}")
 
 
+CASES = {
+    "heis6_p2": lambda: case_exact("heis6_p2", build_model(ModelSpec("heisenberg-chain", n=6)),
+                                   2, (0,)),
+    "hub4_p1": lambda: case_exact("hub4_p1", build_model(ModelSpec("hubbard-chain", n=4, t=1.0,
+                                                                   u=2.0)), 1, (4, 0)),
+    "ints4_p1": lambda: case_exact("ints4_p1", random_integral_model(4, 11), 1, (4, 0)),
+    "ints6_d24_p2": lambda: case_truncated("ints6_d24_p2", random_integral_model(6, 12), 24, 1, 2),
+    # larger truncated case: many sectors, bilinear member blocks, split groups
+    "ints7_d32_p2": lambda: case_truncated("ints7_d32_p2", random_integral_model(7, 13), 32, 1, 2),
+}
+
+
 def main():
-    heis6 = build_model(ModelSpec("heisenberg-chain", n=6))
-    hub4 = build_model(ModelSpec("hubbard-chain", n=4, t=1.0, u=2.0))
-    ints4 = random_integral_model(4, 11)
-    ints6 = random_integral_model(6, 12)
-    cases = [
-        case_exact("heis6_p2", heis6, 2, (0,)),
-        case_exact("hub4_p1", hub4, 1, (4, 0)),
-        case_exact("ints4_p1", ints4, 1, (4, 0)),
-        case_truncated("ints6_d24_p2", ints6, 24, 1, 2),
-    ]
-    for c in cases:
-        record(*c)
+    names = sys.argv[1:] or list(CASES)
+    for name in names:
+        record(*CASES[name]())
 
 
 if __name__ == "__main__":
