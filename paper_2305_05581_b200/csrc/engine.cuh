@@ -104,7 +104,7 @@ struct Seg {         // 40 B
 };
 
 #ifndef SDMRG_STAGES
-#define SDMRG_STAGES 3
+#define SDMRG_STAGES (SDMRG_WIDE ? 4 : 3)
 #endif
 #ifndef SDMRG_TILE
 #define SDMRG_TILE 64
@@ -122,21 +122,27 @@ struct Seg {         // 40 B
 #define SDMRG_LDS128 0
 #endif
 #ifndef SDMRG_MINB
-#define SDMRG_MINB (SDMRG_TILE > 64 ? 2 : 4)
+#define SDMRG_MINB ((SDMRG_TILE > 64 || SDMRG_WIDE) ? 2 : 4)
 #endif
-constexpr int BM = SDMRG_TILE, BN = SDMRG_TILE, BK = 16, STAGES = SDMRG_STAGES;
+// SDMRG_WIDE: 64 x 128 tiles, 8 DMMA warps (2 x 4 grid of <= 32 x 32 warp
+// tiles) per CTA, 2 CTAs per SM — the same 16 DMMA warps per SM as the
+// default, with half the A-panel re-reads between column tiles.
+#ifndef SDMRG_WIDE
+#define SDMRG_WIDE 0
+#endif
+constexpr int BM = SDMRG_TILE, BN = SDMRG_WIDE ? 2 * SDMRG_TILE : SDMRG_TILE, BK = 16;
+constexpr int STAGES = SDMRG_STAGES;
 constexpr int MAXB = BM / 16;                    // 8x8 blocks per warp and dimension
 static_assert(BM == 64 || BM == 96, "tile edge 64 or 96");
-constexpr int CONSUMERS = 4, WGRID_R = 2, WGRID_C = 2;
+constexpr int WGRID_R = 2, WGRID_C = SDMRG_WIDE ? 4 : 2, CONSUMERS = WGRID_R * WGRID_C;
 constexpr int THREADS = 32 * (CONSUMERS + 1);
 constexpr int KC_LD = BK + 2;                    // K-contiguous row stride (144 B)
-constexpr int KC_ELEMS = BM * KC_LD;             // K-contiguous tile (BM == BN)
-constexpr int NC_LD = BM + 4;                    // M/N-contiguous row stride (544 B)
-constexpr int NC_ELEMS = BK * NC_LD;             // M/N-contiguous tile
+constexpr int NC_LD_A = BM + 4;                  // M-contiguous A row stride
+constexpr int NC_LD_B = BN + 4;                  // N-contiguous B row stride
 template <bool TA>
-__host__ __device__ constexpr int a_elems() { return TA ? NC_ELEMS : KC_ELEMS; }
+__host__ __device__ constexpr int a_elems() { return TA ? BK * NC_LD_A : BM * KC_LD; }
 template <bool TB>
-__host__ __device__ constexpr int b_elems() { return TB ? KC_ELEMS : NC_ELEMS; }
+__host__ __device__ constexpr int b_elems() { return TB ? BN * KC_LD : BK * NC_LD_B; }
 template <bool TA, bool TB>
 __host__ __device__ constexpr int stage_elems() { return a_elems<TA>() + b_elems<TB>(); }
 
@@ -247,8 +253,8 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
   constexpr uint32_t STAGE_B = stage_elems<TA, TB>() * 8;
   constexpr int A_I = TA ? 8 * 8 : 8 * KC_LD * 8;         // next 8-row block (bytes)
   constexpr int B_J = TB ? 8 * KC_LD * 8 : 8 * 8;         // next 8-col block
-  constexpr int A_KS = TA ? 4 * NC_LD * 8 : 4 * 8;        // next k4 step
-  constexpr int B_KS = TB ? 4 * 8 : 4 * NC_LD * 8;
+  constexpr int A_KS = TA ? 4 * NC_LD_A * 8 : 4 * 8;      // next k4 step
+  constexpr int B_KS = TB ? 4 * 8 : 4 * NC_LD_B * 8;
   double acc[MB > 0 ? MB : 1][NB > 0 ? NB : 1][2];
 #pragma unroll
   for (int i = 0; i < MB; ++i)
@@ -322,16 +328,16 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
             for (int i = 0; i < MB; ++i) {
               if (!TA) lds128(a0 + h * 64 + i * A_I, ap[i][0], ap[i][1]);
               else {
-                ap[i][0] = lds64(a0 + (8 * h) * NC_LD * 8 + i * A_I);
-                ap[i][1] = lds64(a0 + (8 * h + 1) * NC_LD * 8 + i * A_I);
+                ap[i][0] = lds64(a0 + (8 * h) * NC_LD_A * 8 + i * A_I);
+                ap[i][1] = lds64(a0 + (8 * h + 1) * NC_LD_A * 8 + i * A_I);
               }
             }
 #pragma unroll
             for (int j = 0; j < NB; ++j) {
               if (TB) lds128(b0 + h * 64 + j * B_J, bp[j][0], bp[j][1]);
               else {
-                bp[j][0] = lds64(b0 + (8 * h) * NC_LD * 8 + j * B_J);
-                bp[j][1] = lds64(b0 + (8 * h + 1) * NC_LD * 8 + j * B_J);
+                bp[j][0] = lds64(b0 + (8 * h) * NC_LD_B * 8 + j * B_J);
+                bp[j][1] = lds64(b0 + (8 * h + 1) * NC_LD_B * 8 + j * B_J);
               }
             }
 #pragma unroll
@@ -457,7 +463,7 @@ __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring&
 //     (k, c) at src + k*ld + c.
 // The k tail beyond krem is zero-filled (stale shared memory may hold
 // non-finite data at kernel start).
-template <bool KCONTIG>
+template <bool KCONTIG, int NC_LD, int CAP>
 __device__ __forceinline__ void load_operand_async(uint32_t sbase, const double* src, int ld,
                                                    int extent, int krem, int lane) {
   if (KCONTIG) {
@@ -475,7 +481,7 @@ __device__ __forceinline__ void load_operand_async(uint32_t sbase, const double*
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < BM / 32; ++j) {
+    for (int j = 0; j < CAP / 32; ++j) {
       const int c = lane + 32 * j;
       if (c < extent) {
         const double* p = src + c;
@@ -508,7 +514,7 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const double* gmem, i
 __device__ __forceinline__ void cp_async16_full(uint32_t saddr, const double* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
 }
-template <bool KCONTIG>
+template <bool KCONTIG, int NC_LD, int CAP>
 __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const double* src, int ld,
                                                      int extent, int krem, int lane) {
   if (KCONTIG) {
@@ -528,7 +534,7 @@ __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const doubl
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < (BM + 63) / 64; ++j) {
+    for (int j = 0; j < (CAP + 63) / 64; ++j) {
       const int c = 2 * lane + 64 * j;
       if (c < extent) {
         const double* p = src + c;
@@ -678,11 +684,11 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
         const double* bsrc = TB ? b + k0 : b + (int64_t)k0 * sg.ldb;
 #ifndef SDMRG_EXP_NOLOAD
         if (BULK) {
-          load_operand_aligned<!TA>(sa, asrc, sg.lda, cur.tm, krem, lane);
-          load_operand_aligned<TB>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
+          load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
+          load_operand_aligned<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
         } else {
-          load_operand_async<!TA>(sa, asrc, sg.lda, cur.tm, krem, lane);
-          load_operand_async<TB>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
+          load_operand_async<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
+          load_operand_async<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
         }
 #endif
         __syncwarp();
@@ -761,16 +767,18 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
     // first stage of a tile: balanced 2 x 2 warp split of its 8x8 blocks
     const int tm = m.tm, tn = m.tn;
     const int mb = (tm + 7) >> 3, nb = (tn + 7) >> 3;
-    const int mb0 = (mb + 1) >> 1, nb0 = (nb + 1) >> 1;
+    const int mb0 = (mb + 1) >> 1;
     const int mblk = wr == 0 ? mb0 : mb - mb0;
-    const int nblk = wc == 0 ? nb0 : nb - nb0;
     const int wr0 = wr == 0 ? 0 : mb0 * 8;
-    const int wc0 = wc == 0 ? 0 : nb0 * 8;
+    // columns: balanced over WGRID_C warps
+    const int nbase = nb / WGRID_C, nextra = nb - nbase * WGRID_C;
+    const int nblk = nbase + (wc < nextra ? 1 : 0);
+    const int wc0 = 8 * (wc * nbase + min(wc, nextra));
     // fragment origin: stage k = lc (natural order) or 2 lc (kperm)
     const int kf = SDMRG_LDS128 ? 2 * lc : lc;
-    const uint32_t a_off = TA ? (kf * NC_LD + wr0 + lr) * 8 : ((wr0 + lr) * KC_LD + kf) * 8;
+    const uint32_t a_off = TA ? (kf * NC_LD_A + wr0 + lr) * 8 : ((wr0 + lr) * KC_LD + kf) * 8;
     const uint32_t b_off =
-        A_EL * 8 + (TB ? ((wc0 + lr) * KC_LD + kf) * 8 : (kf * NC_LD + wc0 + lr) * 8);
+        A_EL * 8 + (TB ? ((wc0 + lr) * KC_LD + kf) * 8 : (kf * NC_LD_B + wc0 + lr) * 8);
     double* c = m.c + (int64_t)(wr0 + lr) * m.ldc + wc0 + 2 * lc;
     consume_dispatch<TA, TB>(mblk, nblk, ring, stage, phase, a_off, b_off, c, m.ldc, m.beta,
                              tm - wr0 - lr, tn - wc0 - 2 * lc, lane);
