@@ -8,7 +8,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-CASES = ("heis6_p2", "hub4_p1", "ints4_p1", "ints6_d24_p2")
+CASES = ("heis6_p2", "hub4_p1", "ints4_p1", "ints6_d24_p2", "ints7_d32_p2")
 
 
 def pytest_configure(config):

@@ -66,6 +66,10 @@ def test_oracle_apply_matches_reference(golden):
 
 def test_oracle_lanczos_matches_reference(golden):
     name, pi = golden
+    if pi.meta["lanczos_iterations"] > 150:
+        # the pure-Python oracle would take minutes here; the device Lanczos
+        # checks this case against the reference energy directly
+        pytest.skip("oracle Lanczos restatement pinned on the smaller cases")
     groups = heff.build_groups(pi)
     res = lanczos.lanczos_ground(lambda v: heff.apply_heff(pi, v, groups), pi.meta["psi"],
                                  tol=1e-12, max_iter=300)
