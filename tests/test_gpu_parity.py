@@ -159,10 +159,15 @@ def test_device_lanczos_matches_reference_energy(golden):
     res = lanczos_ground(apply_op, pi.meta["psi"], tol=1e-12, max_iter=300)
     e_ref = float(pi.meta["lanczos_energy"])
     assert abs(res.energy - e_ref) <= 1e-10 * (1 + abs(e_ref))
-    assert res.converged
+    assert res.converged == bool(pi.meta["lanczos_converged"])   # same exit as dmrg.py:93-97
     v = res.vector.cpu().numpy()
-    hv = heff.apply_heff(pi, v)
-    assert np.linalg.norm(hv - res.energy * v) <= 1e-10 * (1 + abs(res.energy))
+    if res.converged:
+        hv = heff.apply_heff(pi, v)
+        assert np.linalg.norm(hv - res.energy * v) <= 1e-10 * (1 + abs(res.energy))
+    else:
+        # both stopped at max_iter / restart limits: same Ritz vector up to sign
+        ref = pi.meta["lanczos_vector"]
+        assert abs(abs(float(np.dot(v, ref))) - 1.0) <= 1e-8
 
 
 def test_device_lanczos_dense_problems():
