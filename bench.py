@@ -458,6 +458,10 @@ def run_b200(args):
                        pi.meta["arena_size_l"] * 8 / 1e9),
                    "psi_size": st["psi_size"], "psi_keys": st["psi_keys"],
                    "groups": st["groups"], "members": st["members"],
+                   "value_basis": "reference FLOP count of one H_eff·psi (plan.flops, "
+                                  "blocks.py:575 / sbmm4s.py:205) per device second: a "
+                                  "time-to-solution rate comparable with --impl reference; "
+                                  "the engine executes fewer FLOPs (exec_tflops, roofline)",
                    "ref_flops_per_step": st["ref_flops"],
                    "exec_flops_per_step_rank0": st["exec_flops"],
                    "phase2_products": st["products"], "combine_outputs": st["combine_outputs"],

@@ -401,9 +401,19 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       ++groups;
       a = b;
     }
-    // sharding cost: the executed phase-2 products of this key
-    for (const Pair& p : pairs[i])
+    // sharding cost: the executed FLOPs of this key — phase-2 products plus
+    // its distinct non-identity T = A R^T (phase 1)
+    std::vector<int32_t> rops;
+    for (const Pair& p : pairs[i]) {
       key_cost[i] += 2.0 * d->dim_l[keys[p.out].jl] * d->dim_r[keys[p.out].jr] * m;
+      if (d->kind_r[p.rop] != 1) rops.push_back(p.rop);
+    }
+    std::sort(rops.begin(), rops.end());
+    rops.erase(std::unique(rops.begin(), rops.end()), rops.end());
+    for (int32_t ro : rops) {
+      const int jrp = shR[(size_t)ro * nR + keys[i].jr];
+      if (jrp >= 0) key_cost[i] += 2.0 * m * n * d->dim_r[jrp];
+    }
   }
   if (d->keep_groups) {
     plan->g_begin.push_back(0);
