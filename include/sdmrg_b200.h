@@ -170,6 +170,9 @@ typedef struct sdmrg_plan_stats {
   int64_t products;                /* phase-2 products (group, right op)      */
   int64_t combine_outputs;         /* pre-summed left operators per apply     */
   int64_t combine_terms;           /* their summands                          */
+  int64_t build_ms_taskgen;        /* host: ψ keys, matching, pre-summation   */
+  int64_t build_ms_emit;           /* host: work lists                        */
+  int64_t build_ms_device;         /* repack, allocations, uploads            */
 } sdmrg_plan_stats;
 
 int sdmrg_plan_build(const sdmrg_plan_desc* desc, sdmrg_plan** out);

@@ -58,7 +58,8 @@ class PlanStats(ctypes.Structure):
         "psi_keys", "psi_size", "groups", "members", "ref_flops", "exec_flops",
         "local_members", "t_problems", "tiles", "segments", "chunks",
         "workspace_doubles", "kernels_per_apply", "algo_bytes", "products",
-        "combine_outputs", "combine_terms")]
+        "combine_outputs", "combine_terms", "build_ms_taskgen", "build_ms_emit",
+        "build_ms_device")]
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

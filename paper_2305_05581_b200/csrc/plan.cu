@@ -25,6 +25,7 @@
 #include <cstring>
 #include <map>
 #include <numeric>
+#include <chrono>
 #include <vector>
 
 #include "../../include/sdmrg_b200.h"
@@ -243,6 +244,12 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   plan->nL = nL;
   plan->nR = nR;
 
+  using clk = std::chrono::steady_clock;
+  const auto t_start = clk::now();
+  auto ms_since = [](clk::time_point t0) {
+    return static_cast<int64_t>(
+        std::chrono::duration_cast<std::chrono::microseconds>(clk::now() - t0).count() / 1000);
+  };
   // ---- ψ keys (blocks.py:416-429): qR = target - qL - q1 - q2 ∈ right basis
   std::map<QN, int> rindex;
   for (int j = 0; j < nR; ++j) rindex[qn_at(d->qn_r, j, nc)] = j;
@@ -510,6 +517,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     }
   }
 
+  const int64_t taskgen_ms = ms_since(t_start);
+  const auto t_emit = clk::now();
   int64_t i0 = d->dry_run ? nk : 0;  // dry run: task generation + stats only
   while (i0 < nk) {
     Chunk ch;
@@ -518,24 +527,39 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       used += t_need[i1];
       ++i1;
     }
-    // phase 1: distinct T per (key, right op)
-    std::vector<std::map<int32_t, std::pair<uint64_t, int>>> tmap(i1 - i0);  // rop -> (handle, ld)
+    // phase 1: distinct T per (key, right op); tmap[i - i0] holds the key's
+    // right ops sorted, with the handle / leading dimension of their T
+    struct TEntry {
+      int32_t rop;
+      int32_t ld;
+      uint64_t handle;
+    };
+    std::vector<std::vector<TEntry>> tmap(i1 - i0);
+    auto t_lookup = [&](int64_t i, int32_t ro) -> const TEntry& {
+      const auto& v = tmap[i - i0];
+      return *std::lower_bound(v.begin(), v.end(), ro,
+                               [](const TEntry& e, int32_t x) { return e.rop < x; });
+    };
     int64_t ws = 0;
     for (int64_t i = i0; i < i1; ++i) {
       if (!mine[i]) continue;
       const Key& k = keys[i];
       const int m = d->dim_l[k.jl], n = d->dim_r[k.jr];
       auto& tm = tmap[i - i0];
-      for (const Pair& pr : pairs[i]) {
-        const int ro = pr.rop;
-        if (tm.count(ro)) continue;
+      std::vector<int32_t> rops;
+      rops.reserve(pairs[i].size());
+      for (const Pair& pr : pairs[i]) rops.push_back(pr.rop);
+      std::sort(rops.begin(), rops.end());
+      rops.erase(std::unique(rops.begin(), rops.end()), rops.end());
+      tm.reserve(rops.size());
+      for (const int32_t ro : rops) {
         if (d->kind_r[ro] == 1) {  // R = identity: T = A (no product)
-          tm[ro] = {make_handle(B_PSI, plan->poffs[i]), pad2(n)};
+          tm.push_back({ro, pad2(n), make_handle(B_PSI, plan->poffs[i])});
           continue;
         }
         const int jrp = shR[(size_t)ro * nR + k.jr];
         const int r = d->dim_r[jrp];
-        tm[ro] = {make_handle(B_WS, ws), pad2(r)};
+        tm.push_back({ro, pad2(r), make_handle(B_WS, ws)});
         ch.host1.begin_prob(make_handle(B_WS, ws), pad2(r), m, r, 0);
         ch.host1.add_seg(make_handle(B_PSI, plan->poffs[i]), pad2(n),
                          make_handle(B_ARENA_R, poff_r[(size_t)ro * nR + k.jr]), pad2(n), n, 1.0);
@@ -549,11 +573,14 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     // phase 0 + 2: one σ problem per out key; one segment per (ψ key, right
     // op) product, ordered (ψ key, rop); multi-term left sums staged by the
     // combine kernel into the workspace after the T blocks
-    std::map<int32_t, std::vector<std::pair<int64_t, const Pair*>>> by_out;
+    std::vector<std::vector<std::pair<int64_t, const Pair*>>> by_out_v(nk);
     for (int64_t i = i0; i < i1; ++i) {
       if (!mine[i]) continue;
-      for (const Pair& pr : pairs[i]) by_out[pr.out].push_back({i, &pr});
+      for (const Pair& pr : pairs[i]) by_out_v[pr.out].push_back({i, &pr});
     }
+    std::vector<std::pair<int32_t, std::vector<std::pair<int64_t, const Pair*>>*>> by_out;
+    for (int64_t o = 0; o < nk; ++o)
+      if (!by_out_v[o].empty()) by_out.push_back({static_cast<int32_t>(o), &by_out_v[o]});
     struct OutProb {
       int32_t o;
       int q, r;
@@ -562,22 +589,23 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     };
     std::vector<OutProb> outs;
     outs.reserve(by_out.size());
-    for (auto& kv : by_out) {
-      const int32_t o = kv.first;
+    for (auto& kvp : by_out) {
+      const int32_t o = kvp.first;
+      const auto& entries = *kvp.second;
       const int q = d->dim_l[keys[o].jl], r = d->dim_r[keys[o].jr];
       OutProb op{o, q, r, 0, {}};
-      for (size_t u = 0; u < kv.second.size();) {
-        const int64_t i = kv.second[u].first;
+      for (size_t u = 0; u < entries.size();) {
+        const int64_t i = entries[u].first;
         const int m = d->dim_l[keys[i].jl];
         const int qm = q * pad2(m);  // a padded q x m block, pads included
         const int32_t out_first = static_cast<int32_t>(ch.comb0.outs.size());
-        for (; u < kv.second.size() && kv.second[u].first == i; ++u) {
-          const Pair& pr = *kv.second[u].second;
+        for (; u < entries.size() && entries[u].first == i; ++u) {
+          const Pair& pr = *entries[u].second;
           const Term* tt = terms[i].data();
-          const auto& th = tmap[i - i0].at(pr.rop);
+          const TEntry& th = t_lookup(i, pr.rop);
           Seg sg{};
-          sg.b = th.first;
-          sg.ldb = th.second;
+          sg.b = th.handle;
+          sg.ldb = th.ld;
           sg.lda = pad2(m);
           sg.k = m;
           if (pr.term_end - pr.term_begin == 1) {
@@ -665,6 +693,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     i0 = i1;
   }
 
+  const int64_t emit_ms = ms_since(t_emit);
+  const auto t_dev = clk::now();
   int64_t ws_max = 0;
   for (auto& ch : plan->chunks) ws_max = std::max(ws_max, ch.ws_doubles);
   rc = SDMRG_OK;
@@ -753,6 +783,9 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     return rc;
   }
   sdmrg_plan_stats& st = plan->stats;
+  st.build_ms_taskgen = taskgen_ms;
+  st.build_ms_emit = emit_ms;
+  st.build_ms_device = ms_since(t_dev);
   st.psi_keys = nk;
   st.psi_size = off;
   st.groups = groups;
