@@ -220,6 +220,13 @@ int upload_vec(const std::vector<T>& v, T** out) {
   return rc;
 }
 
+// Split-K granule = 1/split_factor of one persistent CTA's share of the
+// phase-2 work (SDMRG_SPLIT overrides; experiments).
+double split_factor() {
+  const char* e = getenv("SDMRG_SPLIT");
+  return e ? std::max(1.0, atof(e)) : 96.0;
+}
+
 int launch_combine(const CombList& cl, const Bases& bases, cudaStream_t stream) {
   if (cl.ntasks == 0) return SDMRG_OK;
   combine_kernel<<<static_cast<unsigned>(cl.ntasks), COMB_THREADS, 0, stream>>>(
@@ -639,14 +646,16 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       outs.push_back(std::move(op));
     }
     // split-K for load balance: a σ tile whose K work exceeds the granule
-    // (1/6 of one persistent CTA's share) is cut into contiguous segment
+    // (1/96 of one persistent CTA's share: short tiles keep sibling tiles of one
+    // σ block in step, so their shared operand panels hit in L2 — 1/6 was 5%
+    // slower in phase 2) is cut into contiguous segment
     // ranges written to partial buffers; phase 3 adds them to σ in order
     // (σ first, then parts 0..S-1: deterministic, no atomics).
     auto tiles_of = [](int extent) { return (extent + BM - 1) / BM; };
     double total_cost = 0.0;
     for (const OutProb& op : outs) total_cost += double(op.q) * op.r * op.ksum;
     const double granule =
-        total_cost / (double(d->dry_run ? 1 : engine_grid(false, false)) * 6.0) + 1.0;
+        total_cost / (double(d->dry_run ? 1 : engine_grid(false, false)) * split_factor()) + 1.0;
     for (const OutProb& op : outs) {
       const double tile_cost =
           double(op.q) / tiles_of(op.q) * (double(op.r) / tiles_of(op.r)) * op.ksum;
