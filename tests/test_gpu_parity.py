@@ -316,3 +316,32 @@ def test_plan_apply_edge_cases(golden):
     ref = heff.apply_heff(one, pi.meta["psi"])
     got = DevicePlan(one).apply(psi).cpu().numpy()
     assert rel_err(got, ref) <= 1e-12
+
+
+def test_bench_scale_properties():
+    """At the bench workload (L=30, D=2048): linearity, bitwise determinism,
+    chunked (small workspace) == single-chunk, and the sharded partials sum to
+    the full σ — size-independent checks where the oracle is too slow."""
+    from paper_2305_05581_b200.plan import DevicePlan
+    from paper_2305_05581_b200.workload import fill_arenas_device, synthetic_plan_input
+    pi = synthetic_plan_input(30, 2048, seed=2)
+    al, ar = fill_arenas_device(pi, seed=2)
+    plan = DevicePlan(pi, arena_l=al, arena_r=ar)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(plan.psi_size, generator=g, dtype=torch.float64, device="cuda")
+    y = torch.randn(plan.psi_size, generator=g, dtype=torch.float64, device="cuda")
+    hx, hy = plan.apply(x).clone(), plan.apply(y).clone()
+    hxy = plan.apply(0.5 * x + 2.0 * y)
+    scale = 1.0 + hxy.abs().max().item()
+    assert (hxy - (0.5 * hx + 2.0 * hy)).abs().max().item() <= 1e-12 * scale
+    assert torch.equal(plan.apply(x), hx)
+    chunked = DevicePlan(pi, arena_l=al, arena_r=ar, workspace_doubles=200_000_000)
+    assert chunked.stats["chunks"] > 1
+    assert (chunked.apply(x) - hx).abs().max().item() <= 1e-12 * (1.0 + hx.abs().max().item())
+    chunked.close()
+    parts = torch.zeros_like(hx)
+    for rank in range(2):
+        p = DevicePlan(pi, arena_l=al, arena_r=ar, rank=rank, world=2)
+        parts += p.apply(x)
+        p.close()
+    assert (parts - hx).abs().max().item() <= 1e-12 * (1.0 + hx.abs().max().item())
