@@ -114,6 +114,10 @@ class DevicePlan:
         handle = ctypes.c_void_p()
         _lib.check(lib.sdmrg_plan_build(ctypes.byref(self._desc), ctypes.byref(handle)))
         self._h = handle
+        # the library repacked the arenas into plan-owned padded memory: the
+        # caller's (or our temporary device) copies are no longer referenced
+        self.arena_l = self.arena_r = None
+        self._desc.arena_l = self._desc.arena_r = None
         st = _lib.PlanStats()
         _lib.check(lib.sdmrg_plan_stats_get(self._h, ctypes.byref(st)))
         self.stats = st.as_dict()
