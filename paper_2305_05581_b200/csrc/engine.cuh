@@ -404,19 +404,33 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
     mbar_wait(ring.full0 + 8 * stage, phase);
   }
   // epilogue: masked store (optionally accumulating); row_lim/col_lim are the
-  // tile extents relative to this thread's first row / column
+  // tile extents relative to this thread's first row / column.  A thread's
+  // two accumulators per block are adjacent columns: one 16-byte store when
+  // C is 16-byte aligned with an even leading dimension (the plan's T blocks)
+  const bool vec2 = ((reinterpret_cast<uintptr_t>(c) | (uintptr_t(ldc) << 3)) & 15) == 0;
 #pragma unroll
   for (int i = 0; i < MB; ++i) {
     if (8 * i < row_lim) {
       double* crow = c + (int64_t)(8 * i) * ldc;
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
+        if (vec2 && 8 * j + 1 < col_lim) {
+          double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+          double2* p = reinterpret_cast<double2*>(crow + 8 * j);
+          if (beta) {
+            const double2 o = *p;
+            v.x += o.x;
+            v.y += o.y;
+          }
+          *p = v;
+        } else {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (8 * j + h < col_lim) {
-            double v = acc[i][j][h];
-            if (beta) v += crow[8 * j + h];
-            crow[8 * j + h] = v;
+          for (int h = 0; h < 2; ++h) {
+            if (8 * j + h < col_lim) {
+              double v = acc[i][j][h];
+              if (beta) v += crow[8 * j + h];
+              crow[8 * j + h] = v;
+            }
           }
         }
       }
