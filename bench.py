@@ -154,8 +154,11 @@ def hbm_peak():
 def cpu_sample(pi, plan_groups, keys_order, arena_l, arena_r, budget_s, psi):
     """Reference algorithm (oracle port) on a bounded sample of the groups.
 
-    Times ``oracle.heff.apply_groups`` — dmrg.py:107 per-group sbmm4s with
-    NumPy BLAS — over whole ψ-key group sets until ``budget_s`` elapses.
+    Times ``oracle.heff.apply_groups_threaded`` — dmrg.py:107 per-group
+    sbmm4s, one task per group on a pool of os.cpu_count() host threads with
+    per-output-block locks as the reference's maze-runner pool does, BLAS
+    single-threaded per product — over whole ψ-key group sets until
+    ``budget_s`` elapses.
     Returns (TFLOP/s, seconds, flops, groups done).
     """
     from oracle import heff
@@ -184,7 +187,7 @@ def cpu_sample(pi, plan_groups, keys_order, arena_l, arena_r, budget_s, psi):
             fl += 2 * m * r * n * p + 2 * q * r * m * p
         out = np.zeros_like(psi)
         t0 = time.perf_counter()
-        heff.apply_groups(pi, groups, psi, out)
+        heff.apply_groups_threaded(pi, groups, psi, out)
         t_total += time.perf_counter() - t0
         done_flops += fl
         done_groups += len(groups)
@@ -265,8 +268,9 @@ def run_reference(args):
         "cpu_baseline": {"value": tf, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{len(vals)} samples of ~{per_step:.1f}s each: whole "
                                    f"ψ-key group sets of this workload through "
-                                   f"oracle.heff.apply_groups (reference sbmm4s per group, "
-                                   f"NumPy BLAS); ms_per_step extrapolates the full H_eff·ψ"},
+                                   f"oracle.heff.apply_groups_threaded (reference sbmm4s per "
+                                   f"group on {cores} threads, as its worker pool); "
+                                   f"ms_per_step extrapolates the full H_eff·ψ"},
         "e2e": {"value": tf, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -413,8 +417,9 @@ def run_b200(args):
                                       args.cpu_sample_seconds, hpsi)
         cpu = {"value": tf, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                "sample": f"{ng} of {st['groups']} groups ({fl / st['ref_flops'] * 100:.2f}% of "
-                         f"the step's FLOPs, {secs:.1f}s) through oracle.heff.apply_groups "
-                         f"(reference sbmm4s per group, NumPy BLAS)"}
+                         f"the step's FLOPs, {secs:.1f}s) through "
+                         f"oracle.heff.apply_groups_threaded (reference sbmm4s per group on "
+                         f"{os.cpu_count()} threads, as its worker pool)"}
 
     scale = []
     if world == 1 and args.scale:

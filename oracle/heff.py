@@ -67,28 +67,71 @@ def _block(arena, off, rows, cols):
     return arena[off:off + rows * cols].reshape(rows, cols)
 
 
+def _group_product(pi, keys, offs, grp, psi):
+    """One group's SBMM4S contribution (q x r) — dmrg.py:120-163 body."""
+    i, o, members = grp
+    jl, _s1, _s2, jr = keys[i]
+    m, n = int(pi.dim_l[jl]), int(pi.dim_r[jr])
+    ojl, ojr = keys[o][0], keys[o][3]
+    q, r = int(pi.dim_l[ojl]), int(pi.dim_r[ojr])
+    a = psi[offs[i]:offs[i] + m * n].reshape(m, n)
+    b = np.zeros((q, r))
+    p = len(members)
+    l_stack = np.empty((q, m, p), order="F")                      # dmrg.py:130
+    r_stack = np.empty((r, n, p), order="F")                      # dmrg.py:136
+    for k, (t, s) in enumerate(members):
+        lo, ro = int(pi.lop[t]), int(pi.rop[t])
+        l_stack[:, :, k] = _block(pi.arena_l, int(pi.blk_off_l[lo, jl]), q, m)
+        np.multiply(_block(pi.arena_r, int(pi.blk_off_r[ro, jr]), r, n), s,
+                    out=r_stack[:, :, k])
+    ws = np.zeros(m * p * r)
+    temp = batched_gemm_interleaved(a, r_stack, ws)               # dmrg.py:152
+    concat_gemm_accumulate(l_stack, temp, 1.0, b)                 # dmrg.py:156
+    return b
+
+
 def apply_groups(pi, groups, psi, out=None):
     """out += H_eff psi, group by group, sbmm4s two-step (dmrg.py:120-163)."""
     keys, offs = psi_layout(pi)
     out = np.zeros_like(psi) if out is None else out
-    for i, o, members in groups:
-        jl, _s1, _s2, jr = keys[i]
-        m, n = int(pi.dim_l[jl]), int(pi.dim_r[jr])
-        ojl, ojr = keys[o][0], keys[o][3]
-        q, r = int(pi.dim_l[ojl]), int(pi.dim_r[ojr])
-        a = psi[offs[i]:offs[i] + m * n].reshape(m, n)
-        b = out[offs[o]:offs[o] + q * r].reshape(q, r)
-        p = len(members)
-        l_stack = np.empty((q, m, p), order="F")                  # dmrg.py:130
-        r_stack = np.empty((r, n, p), order="F")                  # dmrg.py:136
-        for k, (t, s) in enumerate(members):
-            lo, ro = int(pi.lop[t]), int(pi.rop[t])
-            l_stack[:, :, k] = _block(pi.arena_l, int(pi.blk_off_l[lo, jl]), q, m)
-            np.multiply(_block(pi.arena_r, int(pi.blk_off_r[ro, jr]), r, n), s,
-                        out=r_stack[:, :, k])
-        ws = np.zeros(m * p * r)
-        temp = batched_gemm_interleaved(a, r_stack, ws)           # dmrg.py:152
-        concat_gemm_accumulate(l_stack, temp, 1.0, b)             # dmrg.py:156
+    for grp in groups:
+        o = grp[1]
+        out[offs[o]:offs[o + 1]] += _group_product(pi, keys, offs, grp, psi).ravel()
+    return out
+
+
+def apply_groups_threaded(pi, groups, psi, out=None, workers=None):
+    """dmrg.py:107 apply_plan with a worker pool: the reference's maze-runner
+    runs one task per group on ``pool.workers`` threads and locks the output
+    block (dmrg.py:158-163).  Same per-group SBMM4S; BLAS single-threaded per
+    call, groups spread over ``workers`` host threads (numpy releases the GIL
+    inside the products).  Accumulation order per output block follows
+    completion order, as in the reference's pool."""
+    import os
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+    keys, offs = psi_layout(pi)
+    out = np.zeros_like(psi) if out is None else out
+    workers = workers or os.cpu_count()
+    locks = {grp[1]: threading.Lock() for grp in groups}
+
+    def run(grp):
+        o = grp[1]
+        b = _group_product(pi, keys, offs, grp, psi).ravel()
+        with locks[o]:
+            out[offs[o]:offs[o + 1]] += b
+
+    try:
+        from threadpoolctl import threadpool_limits
+        ctx = threadpool_limits(limits=1)
+    except ImportError:  # pragma: no cover - threadpoolctl ships in the image
+        ctx = None
+    try:
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            list(ex.map(run, groups))
+    finally:
+        if ctx is not None:
+            ctx.restore_original_limits()
     return out
 
 

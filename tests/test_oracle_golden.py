@@ -193,3 +193,13 @@ def test_native_task_generation_edge_cases(golden):
     zero = _rows_subset(pi, np.ones(pi.nrows, bool))
     zero.alpha = np.zeros_like(zero.alpha)
     assert DevicePlan(zero.normalized(), dry_run=True).stats["members"] == 0
+
+
+def test_oracle_threaded_apply_matches_serial(golden):
+    """The pooled port (bench CPU baseline, the reference's worker-pool
+    semantics) computes the same σ as the serial restatement."""
+    _name, pi = golden
+    groups = heff.build_groups(pi)
+    a = heff.apply_groups(pi, groups, pi.meta["psi"])
+    b = heff.apply_groups_threaded(pi, groups, pi.meta["psi"], workers=4)
+    assert np.max(np.abs(a - b)) <= 1e-13 * (1.0 + np.max(np.abs(a)))
