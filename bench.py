@@ -202,12 +202,12 @@ def scale_point(n_orb, d, seed, peak, applies=3):
     DGEMM peak.  Inputs resident, 1 warm-up, best of ``applies``."""
     import torch
     from paper_2305_05581_b200.plan import DevicePlan
-    from paper_2305_05581_b200.workload import fill_arenas_device, synthetic_plan_input
+    from paper_2305_05581_b200.workload import fill_plan_arenas, synthetic_plan_input
     pi = synthetic_plan_input(n_orb, d, seed=seed)
-    al, ar = fill_arenas_device(pi, seed=seed)
-    plan = DevicePlan(pi, arena_l=al, arena_r=ar)
-    del al, ar
-    torch.cuda.empty_cache()
+    # operators generated straight into the plan's padded arenas: at L=76 a
+    # dense copy beside the padded one would not fit in HBM
+    plan = DevicePlan(pi, empty_arenas=True)
+    fill_plan_arenas(plan, pi, seed=seed)
     st = plan.stats
     psi = torch.randn(plan.psi_size, dtype=torch.float64, device="cuda")
     out = plan.empty_vector()

@@ -18,6 +18,8 @@
  *                                 operator-table rows x ψ sectors -> work list)
  * sdmrg_plan_groups               blocks.py:563 the per-(ψ key, out key) groups
  * sdmrg_plan_shard                (multi-GPU) ψ-sector ownership of a rank
+ * sdmrg_plan_arena                the plan's padded operator arenas (fill in
+ *                                 place: large synthetic workloads)
  * sdmrg_plan_apply                dmrg.py:107  apply_plan (out += H_eff ψ)
  * sdmrg_dot / sdmrg_nrm2 /
  * sdmrg_gemv_t / sdmrg_gemv_n /
@@ -142,7 +144,8 @@ typedef struct sdmrg_plan_desc {
   const int32_t* site2_dst;
   const double* site2_val;
   const double* arena_l;           /* device; repacked into plan-owned padded */
-  const double* arena_r;           /* memory at build (may be freed after)    */
+  const double* arena_r;           /* memory at build (may be freed after);
+                                      NULL: zeroed, fill via sdmrg_plan_arena */
   int64_t workspace_doubles;       /* budget for the T = A R^T staging (0 = auto) */
   int rank;
   int world;
@@ -185,6 +188,14 @@ int sdmrg_plan_layout(const sdmrg_plan* plan, int32_t* keys, int64_t* offsets);
 int sdmrg_plan_groups(const sdmrg_plan* plan, int32_t* group_psi,
                       int32_t* group_out, int64_t* group_begin,
                       int64_t* member_row, double* member_scale);
+/* The plan-owned padded operator arena of one side (0 left, 1 right): device
+ * base pointer, size in doubles, and per (op, column sector) element offsets
+ * (nops * nsec, -1 = absent).  Block (q+δ, q) is dim(q+δ) x dim(q) row-major
+ * with row stride dim(q) rounded up to even; pad columns are zero.  A plan
+ * built with arena_l/arena_r == NULL has zeroed arenas the caller fills in
+ * place through this view (keeping the pads zero) before the first apply.  */
+int sdmrg_plan_arena(const sdmrg_plan* plan, int side, double** base, int64_t* size,
+                     int64_t* offsets);
 /* Shard ownership: mine[i] = 1 when ψ key i is this rank's input sector
  * (psi_keys entries).  Every key belongs to exactly one rank of `world`.    */
 int sdmrg_plan_shard(const sdmrg_plan* plan, int32_t* mine);

@@ -82,6 +82,7 @@ _SIGS = {
     "sdmrg_plan_layout": (c_int, [c_vp, P_i32, P_i64]),
     "sdmrg_plan_groups": (c_int, [c_vp, P_i32, P_i32, P_i64, P_i64, P_dbl]),
     "sdmrg_plan_shard": (c_int, [c_vp, P_i32]),
+    "sdmrg_plan_arena": (c_int, [c_vp, c_int, ctypes.POINTER(c_vp), P_i64, P_i64]),
     "sdmrg_plan_apply": (c_int, [c_vp, c_vp, c_vp, c_int, c_vp]),
     "sdmrg_plan_destroy": (c_int, [c_vp]),
     "sdmrg_plan_set_timing": (c_int, [c_vp, c_int]),

@@ -142,6 +142,8 @@ struct sdmrg_plan {
   int* counters = nullptr;
   double* arena_l = nullptr;       // padded device copies (owned)
   double* arena_r = nullptr;
+  int64_t arena_size[2] = {0, 0};
+  std::vector<int64_t> arena_off[2];  // padded (op, column sector) offsets
   double* psi_pad = nullptr;       // padded ψ, refilled by every apply
   std::vector<int64_t> poffs;      // padded ψ block offsets (psi_keys + 1)
   std::vector<char> mine;          // ψ keys of this rank's shard
@@ -311,12 +313,15 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   }
   // padded arena offsets: block (op, column sector j) has rows dim(j + delta),
   // row stride pad2(dim(j))
+  // column-sector-major: all operators' blocks of column sector j are one
+  // contiguous run of rows with the same row stride pad2(dim(j)) (the R
+  // blocks a ψ key's phase 1 reads sit together; fillers see 2-d runs)
   auto pad_offsets = [](int nops, int nsec, const int64_t* boff, const int32_t* shift,
                         const int32_t* dim, std::vector<int64_t>& out) {
     out.assign((size_t)nops * nsec, -1);
     int64_t pos = 0;
-    for (int o = 0; o < nops; ++o)
-      for (int j = 0; j < nsec; ++j) {
+    for (int j = 0; j < nsec; ++j)
+      for (int o = 0; o < nops; ++o) {
         const size_t x = (size_t)o * nsec + j;
         if (boff[x] < 0 || shift[x] < 0) continue;
         out[x] = pos;
@@ -726,9 +731,10 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       PadList pl;
       if (!r) r = upload_vec(tasks, &pl.d_tasks);
       pl.n = static_cast<int64_t>(tasks.size());
-      if (!r && pl.n > 0) {
-        if (!src) r = fail(SDMRG_EINVAL, "plan: null operator arena");
-        else {
+      // no source arena: the plan owns zeroed padded arenas that the caller
+      // fills in place (sdmrg_plan_arena) — no dense copy ever coexists
+      if (!r && pl.n > 0 && src) {
+        {
           pad_kernel<<<static_cast<unsigned>(std::min<int64_t>(pl.n, 148 * 16)), 256>>>(
               pl.d_tasks, pl.n, src, *out);
           count_launch();
@@ -738,6 +744,10 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       pl.release();
       return r;
     };
+    plan->arena_size[0] = psize_l;
+    plan->arena_size[1] = psize_r;
+    plan->arena_off[0] = poff_l;
+    plan->arena_off[1] = poff_r;
     rc = repack(d->arena_l, d->blk_off_l, poff_l, shL, d->dim_l, d->nops_l, nL, psize_l,
                 &plan->arena_l);
     if (!rc)
@@ -830,6 +840,16 @@ int sdmrg_plan_layout(const sdmrg_plan* plan, int32_t* keys, int64_t* offsets) {
   if (!plan) return fail(SDMRG_EINVAL, "plan_layout: null plan");
   if (keys) std::memcpy(keys, plan->keys.data(), plan->keys.size() * sizeof(int32_t));
   if (offsets) std::memcpy(offsets, plan->offs.data(), plan->offs.size() * sizeof(int64_t));
+  return SDMRG_OK;
+}
+
+int sdmrg_plan_arena(const sdmrg_plan* plan, int side, double** base, int64_t* size,
+                     int64_t* offsets) {
+  if (!plan || (side != 0 && side != 1)) return fail(SDMRG_EINVAL, "plan_arena: bad argument");
+  if (base) *base = side == 0 ? plan->arena_l : plan->arena_r;
+  if (size) *size = plan->arena_size[side];
+  if (offsets)
+    std::copy(plan->arena_off[side].begin(), plan->arena_off[side].end(), offsets);
   return SDMRG_OK;
 }
 

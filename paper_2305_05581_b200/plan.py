@@ -94,7 +94,11 @@ class DevicePlan:
     """
 
     def __init__(self, pi, device=None, rank=0, world=1, workspace_doubles=0,
-                 keep_groups=False, dry_run=False, arena_l=None, arena_r=None):
+                 keep_groups=False, dry_run=False, arena_l=None, arena_r=None,
+                 empty_arenas=False):
+        """``empty_arenas``: the plan allocates zeroed padded arenas that the
+        caller fills in place (``padded_arena``) — for operator sets too large
+        to hold a dense copy beside the padded one."""
         lib = _lib.load()
         self.pi = pi.normalized()
         self.rank, self.world = int(rank), int(world)
@@ -105,10 +109,11 @@ class DevicePlan:
             if torch is None or not torch.cuda.is_available():
                 raise _lib.LibraryError("DevicePlan needs a CUDA device (no CPU fallback)")
             self.device = torch.device(device if device is not None else "cuda")
-            self.arena_l = arena_l if arena_l is not None else \
-                torch.from_numpy(self.pi.arena_l).to(self.device)
-            self.arena_r = arena_r if arena_r is not None else \
-                torch.from_numpy(self.pi.arena_r).to(self.device)
+            if not empty_arenas:
+                self.arena_l = arena_l if arena_l is not None else \
+                    torch.from_numpy(self.pi.arena_l).to(self.device)
+                self.arena_r = arena_r if arena_r is not None else \
+                    torch.from_numpy(self.pi.arena_r).to(self.device)
         self._desc = _desc(self.pi, self.arena_l, self.arena_r, rank, world,
                            workspace_doubles, keep_groups, dry_run)
         handle = ctypes.c_void_p()
@@ -154,6 +159,25 @@ class DevicePlan:
             self._h, P(gp, ctypes.c_int32), P(go, ctypes.c_int32), P(gb, ctypes.c_int64),
             P(mr, ctypes.c_int64), P(ms, ctypes.c_double)))
         return PlanGroups(gp, go, gb, mr, ms)
+
+    def padded_arena(self, side):
+        """(CUDA tensor view of the plan-owned padded arena, offsets[nops, nsec])
+        for side 'l' or 'r' (sdmrg_plan_arena)."""
+        k = {"l": 0, "r": 1}[side]
+        nops = self.pi.kind_l.shape[0] if k == 0 else self.pi.kind_r.shape[0]
+        nsec = self.pi.dim_l.shape[0] if k == 0 else self.pi.dim_r.shape[0]
+        base = ctypes.c_void_p()
+        size = ctypes.c_int64()
+        offs = np.zeros((nops, nsec), np.int64)
+        _lib.check(_lib.load().sdmrg_plan_arena(self._h, k, ctypes.byref(base),
+                                                ctypes.byref(size),
+                                                _lib.as_p(offs, ctypes.c_int64)))
+
+        class _View:  # zero-copy device view (CUDA array interface)
+            __cuda_array_interface__ = {"shape": (int(size.value),), "typestr": "<f8",
+                                        "data": (int(base.value or 0), False), "version": 3}
+        view = torch.as_tensor(_View(), device=self.device)
+        return view, offs
 
     def shard(self):
         """Boolean mask over ψ keys: the input sectors this rank applies."""

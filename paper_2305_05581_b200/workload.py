@@ -145,3 +145,51 @@ def _identities(pi, side, arena):
                 blk = arena[off:off + n * n].view(n, n)
                 blk.zero_()
                 blk.fill_diagonal_(1.0)
+
+
+def fill_plan_arenas(plan, pi, seed=0):
+    """Fill a plan built with ``empty_arenas=True`` in place: seeded normal
+    blocks (scale 1/8), identity ops exact, pad columns zero.  The padded
+    arenas are column-sector-major (sdmrg_plan_arena), so each column sector's
+    blocks form one (rows x even stride) run filled by two tensor ops — no
+    dense copy of the operators ever exists beside the padded one."""
+    import torch
+    g = torch.Generator(device=plan.device)
+    g.manual_seed(seed)
+    for side in ("l", "r"):
+        view, offs = plan.padded_arena(side)
+        dim = pi.dim_l if side == "l" else pi.dim_r
+        kind = pi.kind_l if side == "l" else pi.kind_r
+        for j in range(offs.shape[1]):
+            col = offs[:, j]
+            present = col >= 0
+            if not present.any():
+                continue
+            ld = int(dim[j]) + (int(dim[j]) & 1)
+            lo = int(col[present].min())
+            # run end: last block's offset + its rows * ld
+            hi_op = int(np.argmax(np.where(present, col, -1)))
+            rows_last = _rows_of(pi, side, hi_op, j)
+            hi = int(col[hi_op]) + rows_last * ld
+            run = view[lo:hi].view(-1, ld)
+            run.normal_(generator=g).mul_(0.125)
+            if int(dim[j]) & 1:
+                run[:, -1].zero_()
+            for o in np.nonzero((kind == 1) & present)[0]:
+                n = int(dim[j])
+                blk = view[int(col[o]):int(col[o]) + n * ld].view(n, ld)
+                blk.zero_()
+                blk[:, :n].fill_diagonal_(1.0)
+    torch.cuda.synchronize()
+
+
+def _rows_of(pi, side, op, j):
+    """Row count of block (op, column sector j): dim of sector j + delta(op)."""
+    qn = pi.qn_l if side == "l" else pi.qn_r
+    dim = pi.dim_l if side == "l" else pi.dim_r
+    delta = (pi.delta_l if side == "l" else pi.delta_r)[op]
+    target = tuple(int(a) + int(b) for a, b in zip(qn[j], delta))
+    for k, q in enumerate(qn.tolist()):
+        if tuple(q) == target:
+            return int(dim[k])
+    raise ValueError("block without a row sector")
