@@ -112,6 +112,9 @@ struct Seg {         // 40 B
 #ifndef SDMRG_DB
 #define SDMRG_DB 0
 #endif
+#ifndef SDMRG_STCS
+#define SDMRG_STCS 0
+#endif
 // K order inside a stage (same for both operands, so any bijection is
 // exact): DMMA k4 step ks, thread column lc reads stage k
 //   kperm(ks, lc) = 8 (ks >> 1) + 2 lc + (ks & 1)
@@ -423,8 +426,17 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
             const double2 o = *p;
             v.x += o.x;
             v.y += o.y;
+            *p = v;
+          } else {
+#if SDMRG_STCS
+            // overwrite-only outputs (the T blocks: 32 GB per apply, read
+            // back much later) are streamed: evict-first in L2, so they do
+            // not push out the operand panels the running tiles re-read
+            __stcs(p, v);
+#else
+            *p = v;
+#endif
           }
-          *p = v;
         } else {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
