@@ -142,6 +142,25 @@ def ncu_traffic(kernel, args):
         return None
 
 
+def ncu_counters(args):
+    """Per-engine-phase ncu counters of the committed capture (DMMA-pipe
+    activity, DRAM GB/s against the HBM peak), default workload only."""
+    if (args.L, args.D) != (30, 2048):
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            raw = json.load(fh).get("ncu", {})
+    except (OSError, ValueError):
+        return None
+    out = {}
+    for k, v in raw.items():
+        gbs = (v["dram_read_gb"] + v["dram_write_gb"]) / (v["duration_ms"] * 1e-3)
+        out[k] = {"dmma_pipe_active_pct": v["dmma_pipe_active_pct"], "dram_gbs": round(gbs, 1),
+                  "dram_frac_of_peak": round(gbs / hbm_peak(), 3), "l2_hit_pct": v["l2_hit_pct"],
+                  "source": "profiles/traffic.json (ncu --set full, one launch)"}
+    return out
+
+
 def hbm_peak():
     """HBM roofline denominator: MEASURED_PEAKS.json, else the recipe fallback."""
     try:
@@ -449,7 +468,8 @@ def run_b200(args):
                  "peak_source": ("measured live: cuBLAS DGEMM 8192^3 burst (torch.matmul f64)"
                                  if dom in (1, 2) else "MEASURED_PEAKS.json hbm_gbs"),
                  "phase_ms": phase_ms, "phase_exec_flops": phase_flops,
-                 "phase_bytes": phase_bytes})
+                 "phase_bytes": phase_bytes,
+                 "ncu": ncu_counters(args) if world == 1 else None})
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

@@ -138,7 +138,14 @@ constexpr int STAGES = SDMRG_STAGES;
 constexpr int MAXB = BM / 16;                    // 8x8 blocks per warp and dimension
 static_assert(BM == 64 || BM == 96, "tile edge 64 or 96");
 constexpr int WGRID_R = 2, WGRID_C = SDMRG_WIDE ? 4 : 2, CONSUMERS = WGRID_R * WGRID_C;
-constexpr int THREADS = 32 * (CONSUMERS + 1);
+// SDMRG_PRODUCERS=2: one producer warp per operand (A loader leads the tile
+// queue, the B loader follows through shared memory and a named barrier)
+#ifndef SDMRG_PRODUCERS
+#define SDMRG_PRODUCERS 1
+#endif
+constexpr int PRODUCERS = SDMRG_PRODUCERS;
+static_assert(PRODUCERS == 1 || PRODUCERS == 2, "one or two producer warps");
+constexpr int THREADS = 32 * (CONSUMERS + PRODUCERS);
 constexpr int KC_LD = BK + 2;                    // K-contiguous row stride (144 B)
 constexpr int NC_LD_A = BM + 4;                  // M-contiguous A row stride
 constexpr int NC_LD_B = BN + 4;                  // N-contiguous B row stride
@@ -164,7 +171,7 @@ constexpr int kFirst = 1, kLast = 2, kEnd = 4;
 template <bool TA, bool TB>
 __host__ __device__ constexpr int smem_bytes() {
   return STAGES * stage_elems<TA, TB>() * 8 + STAGES * (int)sizeof(StageMeta) + 2 * STAGES * 8 +
-         kMaxBases * 8;
+         kMaxBases * 8 + 16;
 }
 
 __device__ __forceinline__ void cp_async8(uint32_t saddr, const double* gmem, bool valid) {
@@ -617,13 +624,15 @@ template <bool TA, bool TB, bool BULK>
 __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restrict__ tiles,
                                         int ntiles, const Seg* __restrict__ segs,
                                         int* __restrict__ counter, double* const* sbases,
-                                        int lane) {
+                                        int lane, int role, volatile int* s_next) {
+  // role 0: the only producer; 1: A loader + tile-queue leader; 2: B loader
+  const bool load_a = role != 2, load_b = role != 1, leader = role != 2;
   constexpr int A_EL = a_elems<TA>();
   constexpr uint32_t STAGE_B = stage_elems<TA, TB>() * 8;
   // lane 0 writes the stage metadata; the arrive publishes it (release)
   auto meta_write = [&](int stage, int nks, double scale, int flags, const TileRec& tr,
                         double* cptr) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       StageMeta& m = ring.meta[stage];
       m.nks = nks;
       m.scale = scale;
@@ -640,7 +649,15 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
   auto publish_empty = [&](int stage) {  // a stage without operand data
     __syncwarp();
     mbar_arrive_cp_async(ring.full0 + 8 * stage);
-    if (lane == 0) mbar_arrive(ring.full0 + 8 * stage);
+    if (lane == 0 && leader) mbar_arrive(ring.full0 + 8 * stage);
+  };
+  // tile indices: the leader claims, a follower reads them from s_next
+  auto share = [&](int& v, int slot) {
+    if (PRODUCERS == 1) return;
+    if (role == 1 && lane == 0) s_next[slot] = v;
+    asm volatile("bar.sync 1, 64;\n" ::: "memory");
+    if (role == 2) v = s_next[slot];
+    asm volatile("bar.sync 1, 64;\n" ::: "memory");
   };
   int stage = 0;
   uint32_t phase = 0;
@@ -649,12 +666,14 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
   // neither the atomic nor the dependent descriptor load sits on the path
   // between two tiles (consumers measured waiting at tile starts otherwise).
   int t = 0, t1 = 0;
-  if (lane == 0) {
+  if (lane == 0 && leader) {
     t = atomicAdd(counter, 1);
     t1 = atomicAdd(counter, 1);
   }
   t = __shfl_sync(0xffffffffu, t, 0);
   t1 = __shfl_sync(0xffffffffu, t1, 0);
+  share(t, 0);
+  share(t1, 1);
   TileRec cur{}, nrec{};
   Seg sn{};                       // prefetched next segment descriptor
   if (t < ntiles) {
@@ -664,7 +683,7 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
   if (t1 < ntiles) nrec = tiles[t1];
   while (t < ntiles) {
     int t2 = 0;
-    if (lane == 0) t2 = atomicAdd(counter, 1);  // resolved by the end of this tile
+    if (lane == 0 && leader) t2 = atomicAdd(counter, 1);  // resolved by the tile's end
     const int next = t1;
     double* cptr = sbases[cur.c >> kHandleShift] + (cur.c & kHandleMask) +
                    (int64_t)cur.row0 * cur.ldc + cur.col0;
@@ -712,16 +731,16 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
         const double* bsrc = TB ? b + k0 : b + (int64_t)k0 * sg.ldb;
 #ifndef SDMRG_EXP_NOLOAD
         if (BULK) {
-          load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
-          load_operand_aligned<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
+          if (load_a) load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
+          if (load_b) load_operand_aligned<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
         } else {
-          load_operand_async<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
-          load_operand_async<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
+          if (load_a) load_operand_async<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
+          if (load_b) load_operand_async<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
         }
 #endif
         __syncwarp();
         mbar_arrive_cp_async(full);
-        if (lane == 0) mbar_arrive(full);
+        if (lane == 0 && leader) mbar_arrive(full);
         first = false;
         if (++stage == STAGES) {
           stage = 0;
@@ -730,6 +749,7 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
       }
     }
     t2 = __shfl_sync(0xffffffffu, t2, 0);
+    share(t2, 0);
     TileRec n2{};
     if (t2 < ntiles) n2 = tiles[t2];
     t = next;
@@ -759,6 +779,7 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
   StageMeta* meta = reinterpret_cast<StageMeta*>(smem + STAGES * stage_elems<TA, TB>());
   uint64_t* bars = reinterpret_cast<uint64_t*>(meta + STAGES);   // full[STAGES], empty[STAGES]
   double** sbases = reinterpret_cast<double**>(bars + 2 * STAGES);
+  volatile int* s_next = reinterpret_cast<volatile int*>(sbases + kMaxBases);
   Ring ring;
   ring.smem = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   ring.full0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
@@ -771,15 +792,16 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
 #pragma unroll
     for (int k = 0; k < kMaxBases; ++k) sbases[k] = bases.p[k];
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(ring.full0 + 8 * s, 33);          // 32 cp.async arrivals + the meta arrive
+      mbar_init(ring.full0 + 8 * s, 32 * PRODUCERS + 1);  // cp.async arrivals + meta arrive
       mbar_init(ring.empty0 + 8 * s, CONSUMERS);  // one arrive per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == CONSUMERS) {
-    produce<TA, TB, BULK>(ring, tiles, ntiles, segs, counter, sbases, lane);
+  if (warp >= CONSUMERS) {
+    const int role = PRODUCERS == 1 ? 0 : (warp == CONSUMERS ? 1 : 2);
+    produce<TA, TB, BULK>(ring, tiles, ntiles, segs, counter, sbases, lane, role, s_next);
     return;
   }
 
