@@ -552,7 +552,11 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       return *std::lower_bound(v.begin(), v.end(), ro,
                                [](const TEntry& e, int32_t x) { return e.rop < x; });
     };
-    int64_t ws = 0;
+    // parallel over keys: per-key T tables and problem lists, workspace
+    // offsets from a prefix sum, merged in key order (deterministic)
+    const int64_t nkc = i1 - i0;
+    std::vector<int64_t> ws_key(nkc + 1, 0);
+#pragma omp parallel for schedule(dynamic, 8)
     for (int64_t i = i0; i < i1; ++i) {
       if (!mine[i]) continue;
       const Key& k = keys[i];
@@ -564,24 +568,45 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       std::sort(rops.begin(), rops.end());
       rops.erase(std::unique(rops.begin(), rops.end()), rops.end());
       tm.reserve(rops.size());
+      int64_t need = 0;
       for (const int32_t ro : rops) {
         if (d->kind_r[ro] == 1) {  // R = identity: T = A (no product)
           tm.push_back({ro, pad2(n), make_handle(B_PSI, plan->poffs[i])});
           continue;
         }
-        const int jrp = shR[(size_t)ro * nR + k.jr];
-        const int r = d->dim_r[jrp];
-        tm.push_back({ro, pad2(r), make_handle(B_WS, ws)});
-        ch.host1.begin_prob(make_handle(B_WS, ws), pad2(r), m, r, 0);
-        ch.host1.add_seg(make_handle(B_PSI, plan->poffs[i]), pad2(n),
-                         make_handle(B_ARENA_R, poff_r[(size_t)ro * nR + k.jr]), pad2(n), n, 1.0);
-        ch.host1.end_prob();
-        ws += (int64_t)m * pad2(r);
-        exec_flops += 2LL * m * n * r;
-        ch.flops1 += 2LL * m * n * r;
-        ++t_problems;
+        const int r = d->dim_r[shR[(size_t)ro * nR + k.jr]];
+        tm.push_back({ro, pad2(r), make_handle(B_WS, need)});  // relative; rebased below
+        need += (int64_t)m * pad2(r);
+      }
+      ws_key[i - i0 + 1] = need;
+    }
+    for (int64_t x = 0; x < nkc; ++x) ws_key[x + 1] += ws_key[x];
+    std::vector<GemmBatch> p1key(nkc);
+    int64_t f1 = 0, np1 = 0;
+#pragma omp parallel for schedule(dynamic, 8) reduction(+ : f1, np1)
+    for (int64_t i = i0; i < i1; ++i) {
+      if (!mine[i]) continue;
+      const Key& k = keys[i];
+      const int m = d->dim_l[k.jl], n = d->dim_r[k.jr];
+      GemmBatch& gb = p1key[i - i0];
+      for (TEntry& te : tmap[i - i0]) {
+        if (d->kind_r[te.rop] == 1) continue;
+        te.handle = make_handle(B_WS, ws_key[i - i0] + (int64_t)(te.handle & kHandleMask));
+        const int r = d->dim_r[shR[(size_t)te.rop * nR + k.jr]];
+        gb.begin_prob(te.handle, pad2(r), m, r, 0);
+        gb.add_seg(make_handle(B_PSI, plan->poffs[i]), pad2(n),
+                   make_handle(B_ARENA_R, poff_r[(size_t)te.rop * nR + k.jr]), pad2(n), n, 1.0);
+        gb.end_prob();
+        f1 += 2LL * m * n * r;
+        ++np1;
       }
     }
+    for (auto& gb : p1key) ch.host1.append(std::move(gb));
+    p1key.clear();
+    int64_t ws = ws_key[nkc];
+    exec_flops += f1;
+    ch.flops1 += f1;
+    t_problems += np1;
     // phase 0 + 2: one σ problem per out key; one segment per (ψ key, right
     // op) product, ordered (ψ key, rop); multi-term left sums staged by the
     // combine kernel into the workspace after the T blocks

@@ -106,6 +106,23 @@ void GemmBatch::end_prob() {
     }
 }
 
+void GemmBatch::append(GemmBatch&& o) {
+  const int32_t pbase = static_cast<int32_t>(probs.size());
+  const int32_t sbase = static_cast<int32_t>(segs.size());
+  for (Prob p : o.probs) {
+    p.seg_begin += sbase;
+    p.seg_end += sbase;
+    probs.push_back(p);
+  }
+  segs.insert(segs.end(), o.segs.begin(), o.segs.end());
+  for (Tile t : o.tiles) {
+    t.prob += pbase;
+    tiles.push_back(t);
+  }
+  tile_cost.insert(tile_cost.end(), o.tile_cost.begin(), o.tile_cost.end());
+  o = GemmBatch();
+}
+
 void GemmBatch::finalize_tiles() {
   // stable descending-cost order by bucketing on the (few) distinct costs:
   // O(n + u log u) instead of a comparison sort of millions of tiles

@@ -34,6 +34,8 @@ struct GemmBatch {
   std::vector<Tile> tiles;
   std::vector<double> tile_cost;
   int begin_prob(uint64_t c, int ldc, int m, int n, int beta);
+  // move another batch's problems, segments and tiles behind this one's
+  void append(GemmBatch&& other);
   void add_seg(uint64_t a, int lda, uint64_t b, int ldb, int k, double scale);
   void end_prob();
   // order tiles by descending cost (longest-processing-time first)
