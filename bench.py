@@ -215,14 +215,14 @@ def cpu_sample(pi, plan_groups, keys_order, arena_l, arena_r, budget_s, psi):
     return done_flops / t_total / 1e12, t_total, done_flops, done_groups
 
 
-def scale_point(n_orb, d, seed, peak, applies=3):
+def scale_point(n_orb, d, seed, peak, applies=3, n_elec=None):
     """One H_eff·ψ at a larger bond dimension (north star: D >= 4096): device
     ms per apply, reference TFLOP/s, engine TFLOP/s and its fraction of the
     DGEMM peak.  Inputs resident, 1 warm-up, best of ``applies``."""
     import torch
     from paper_2305_05581_b200.plan import DevicePlan
     from paper_2305_05581_b200.workload import fill_plan_arenas, synthetic_plan_input
-    pi = synthetic_plan_input(n_orb, d, seed=seed)
+    pi = synthetic_plan_input(n_orb, d, seed=seed, n_elec=n_elec)
     # operators generated straight into the plan's padded arenas: at L=76 a
     # dense copy beside the padded one would not fit in HBM
     plan = DevicePlan(pi, empty_arenas=True)
