@@ -79,10 +79,11 @@ struct Prob {        // 32 B
   int32_t seg_begin, seg_end;
   int32_t beta;      // 1: accumulate into C, 0: overwrite
 };
-struct Tile {        // 16 B
+struct Tile {        // host only
   int32_t prob;
   int32_t row0, col0;
   int16_t tm, tn;    // tile extents (<= 128)
+  int32_t colw;      // the problem's column-tile width (stage-tiled B operands)
 };
 // Device form of a tile: the problem fields folded in, so the producer needs
 // one dependent load (tile -> segment) instead of two.
@@ -92,14 +93,18 @@ struct TileRec {     // 40 B
   int32_t seg_begin, seg_end;
   int32_t row0, col0;
   int16_t tm, tn;
-  int32_t pad;
+  int32_t colw;      // column-tile width of the problem (stage-tiled B)
 };
 struct Seg {         // 40 B
   uint64_t a;        // handle of opA(0,0)
   uint64_t b;        // handle of opB(0,0)
   int32_t lda, ldb;
   int32_t k;         // > 0 (empty segments are never emitted)
-  int32_t pad;
+  // > 0: B is stage-tiled (M/N-contiguous B only): column tile ct of the
+  // problem is a contiguous [btile rows = K rounded up to 16][NC_LD_B] block
+  // at b + ct * btile * NC_LD_B, so one K stage is ONE contiguous run (a TMA
+  // bulk copy); rows >= K are zero.  ldb must be NC_LD_B.
+  int32_t btile;
   double scale;
 };
 
@@ -716,7 +721,9 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
       const double* b = sbases[sg.b >> kHandleShift] + (sg.b & kHandleMask);
       // operand origins at this tile: A rows row0.., B cols col0..
       a += TA ? cur.row0 : (int64_t)cur.row0 * sg.lda;
-      b += TB ? (int64_t)cur.col0 * sg.ldb : cur.col0;
+      const bool btiled = !TB && BULK && sg.btile > 0;
+      if (btiled) b += (int64_t)(cur.col0 / cur.colw) * sg.btile * NC_LD_B;
+      else b += TB ? (int64_t)cur.col0 * sg.ldb : cur.col0;
       for (int k0 = 0; k0 < sg.k; k0 += BK) {
         const int krem = min(BK, sg.k - k0);
         mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
@@ -730,7 +737,17 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
         const double* asrc = TA ? a + (int64_t)k0 * sg.lda : a + k0;
         const double* bsrc = TB ? b + k0 : b + (int64_t)k0 * sg.ldb;
 #ifndef SDMRG_EXP_NOLOAD
-        if (BULK) {
+        if (btiled) {
+          // the whole B stage is one contiguous [16][NC_LD_B] run: lane 0
+          // registers its bytes and issues one TMA-unit bulk copy (its
+          // expect_tx arrive stands in for the meta arrive)
+          __syncwarp();
+          if (lane == 0 && load_b) {
+            mbar_arrive_expect_tx(full, BK * NC_LD_B * 8);
+            bulk_copy(sb, bsrc, BK * NC_LD_B * 8, full);
+          }
+          if (load_a) load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
+        } else if (BULK) {
           if (load_a) load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
           if (load_b) load_operand_aligned<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
         } else {
@@ -740,7 +757,7 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
 #endif
         __syncwarp();
         mbar_arrive_cp_async(full);
-        if (lane == 0 && leader) mbar_arrive(full);
+        if (lane == 0 && leader && !btiled) mbar_arrive(full);
         first = false;
         if (++stage == STAGES) {
           stage = 0;

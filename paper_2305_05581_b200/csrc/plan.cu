@@ -41,7 +41,18 @@ namespace {
 // (even leading dimensions, even element offsets, zero pads): the operator
 // arenas (repacked once at build), ψ (copied per apply) and the workspace.
 // σ is only written (epilogue) and keeps the reference layout.
-enum { B_PSI = 0, B_SIGMA = 1, B_ARENA_L = 2, B_ARENA_R = 3, B_WS = 4 };
+enum { B_PSI = 0, B_SIGMA = 1, B_ARENA_L = 2, B_ARENA_R = 3, B_WS = 4, B_PSIT = 5 };
+
+// Stage-tiled T (phase 2's B operand): T(i, b) (m x r) is stored as column
+// tiles of the σ problems' width w = col_tile_width(r), each a contiguous
+// [pad16(m)][NC_LD_B] block, so every 16-deep K stage of phase 2 is one
+// contiguous run fetched by a single bulk copy.  Identity right ops read ψ in
+// the same form (psi_tiled, refilled per apply).
+inline int pad16(int x) { return (x + 15) & ~15; }
+inline int64_t tiled_size(int m, int r) {
+  const int w = GemmBatch::col_tile_width(r);
+  return (int64_t)((r + w - 1) / w) * pad16(m) * NC_LD_B;
+}
 
 inline int pad2(int x) { return x + (x & 1); }
 
@@ -148,6 +159,10 @@ struct sdmrg_plan {
   std::vector<int64_t> poffs;      // padded ψ block offsets (psi_keys + 1)
   std::vector<char> mine;          // ψ keys of this rank's shard
   PadList psi_copy;                // ψ -> psi_pad block list (device)
+  PadList psit_copy;               // ψ -> psi_tiled (stage-tiled ψ, phase 2 B)
+  double* psi_tiled = nullptr;
+  std::vector<int64_t> ptoffs;     // psi_tiled block offsets
+  bool tiled = false;
   // optional (SDMRG_SIDE_STREAM=1): phase 0 (combine) on a low-priority side
   // stream concurrently with phase 1 (it only needs the L arena).  Measured
   // no gain at L=30 D=2048 (99.0 vs 99.4 ms, same box), and it blurs the
@@ -311,6 +326,11 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     }
     plan->poffs[nk] = po;
   }
+  plan->tiled = !d->dry_run && getenv("SDMRG_TILED_T") != nullptr;
+  plan->ptoffs.assign(nk + 1, 0);
+  for (int64_t i = 0; i < nk; ++i)
+    plan->ptoffs[i + 1] =
+        plan->ptoffs[i] + tiled_size(d->dim_l[keys[i].jl], d->dim_r[keys[i].jr]);
   // padded arena offsets: block (op, column sector j) has rows dim(j + delta),
   // row stride pad2(dim(j))
   // column-sector-major: all operators' blocks of column sector j are one
@@ -488,7 +508,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     for (int32_t ro : rops) {
       if (d->kind_r[ro] == 1) continue;
       const int jrp = shR[(size_t)ro * nR + keys[i].jr];
-      t_need[i] += m * pad2(d->dim_r[jrp]);
+      t_need[i] += plan->tiled ? tiled_size((int)m, d->dim_r[jrp]) : m * pad2(d->dim_r[jrp]);
     }
   }
   int64_t total_t = 0;
@@ -545,6 +565,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       int32_t rop;
       int32_t ld;
       uint64_t handle;
+      int32_t btile;  // > 0: stage-tiled T (phase 2 B operand)
     };
     std::vector<std::vector<TEntry>> tmap(i1 - i0);
     auto t_lookup = [&](int64_t i, int32_t ro) -> const TEntry& {
@@ -571,12 +592,20 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       int64_t need = 0;
       for (const int32_t ro : rops) {
         if (d->kind_r[ro] == 1) {  // R = identity: T = A (no product)
-          tm.push_back({ro, pad2(n), make_handle(B_PSI, plan->poffs[i])});
+          if (plan->tiled)
+            tm.push_back({ro, NC_LD_B, make_handle(B_PSIT, plan->ptoffs[i]), pad16(m)});
+          else
+            tm.push_back({ro, pad2(n), make_handle(B_PSI, plan->poffs[i]), 0});
           continue;
         }
         const int r = d->dim_r[shR[(size_t)ro * nR + k.jr]];
-        tm.push_back({ro, pad2(r), make_handle(B_WS, need)});  // relative; rebased below
-        need += (int64_t)m * pad2(r);
+        if (plan->tiled) {
+          tm.push_back({ro, NC_LD_B, make_handle(B_WS, need), pad16(m)});  // rebased below
+          need += tiled_size(m, r);
+        } else {
+          tm.push_back({ro, pad2(r), make_handle(B_WS, need), 0});  // relative; rebased below
+          need += (int64_t)m * pad2(r);
+        }
       }
       ws_key[i - i0 + 1] = need;
     }
@@ -591,12 +620,25 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       GemmBatch& gb = p1key[i - i0];
       for (TEntry& te : tmap[i - i0]) {
         if (d->kind_r[te.rop] == 1) continue;
-        te.handle = make_handle(B_WS, ws_key[i - i0] + (int64_t)(te.handle & kHandleMask));
+        const int64_t base = ws_key[i - i0] + (int64_t)(te.handle & kHandleMask);
+        te.handle = make_handle(B_WS, base);
         const int r = d->dim_r[shR[(size_t)te.rop * nR + k.jr]];
-        gb.begin_prob(te.handle, pad2(r), m, r, 0);
-        gb.add_seg(make_handle(B_PSI, plan->poffs[i]), pad2(n),
-                   make_handle(B_ARENA_R, poff_r[(size_t)te.rop * nR + k.jr]), pad2(n), n, 1.0);
-        gb.end_prob();
+        const uint64_t rblk = make_handle(B_ARENA_R, poff_r[(size_t)te.rop * nR + k.jr]);
+        if (te.btile > 0) {
+          // one problem per column tile of T, written as its [pad16(m)][NC_LD_B] block
+          const int w = GemmBatch::col_tile_width(r);
+          for (int c0 = 0, ct = 0; c0 < r; c0 += w, ++ct) {
+            gb.begin_prob(make_handle(B_WS, base + (int64_t)ct * te.btile * NC_LD_B), NC_LD_B, m,
+                          std::min(w, r - c0), 0);
+            gb.add_seg(make_handle(B_PSI, plan->poffs[i]), pad2(n),
+                       rblk + (uint64_t)((int64_t)c0 * pad2(n)), pad2(n), n, 1.0);
+            gb.end_prob();
+          }
+        } else {
+          gb.begin_prob(te.handle, pad2(r), m, r, 0);
+          gb.add_seg(make_handle(B_PSI, plan->poffs[i]), pad2(n), rblk, pad2(n), n, 1.0);
+          gb.end_prob();
+        }
         f1 += 2LL * m * n * r;
         ++np1;
       }
@@ -643,6 +685,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
           Seg sg{};
           sg.b = th.handle;
           sg.ldb = th.ld;
+          sg.btile = th.btile;
           sg.lda = pad2(m);
           sg.k = m;
           if (pr.term_end - pr.term_begin == 1) {
@@ -695,7 +738,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       const uint64_t sig = make_handle(B_SIGMA, plan->offs[op.o]);
       if (nsplit == 1) {
         ch.host2.begin_prob(sig, op.r, op.q, op.r, 1);
-        for (const Seg& sg : op.segs) ch.host2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale);
+        for (const Seg& sg : op.segs)
+          ch.host2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale, sg.btile);
         ch.host2.end_prob();
         continue;
       }
@@ -711,7 +755,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
         ch.host2.begin_prob(part, op.r, op.q, op.r, 0);
         do {
           const Seg& sg = op.segs[u++];
-          ch.host2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale);
+          ch.host2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale, sg.btile);
           kdone += sg.k;
         } while (u < op.segs.size() && (kdone < kcut || sp == nsplit - 1));
         ch.host2.end_prob();
@@ -788,6 +832,21 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     }
     if (!rc) rc = upload_vec(ptasks, &plan->psi_copy.d_tasks);
     plan->psi_copy.n = static_cast<int64_t>(ptasks.size());
+    if (!rc && plan->tiled) {
+      const int64_t pt = std::max<int64_t>(plan->ptoffs[nk], 2);
+      rc = cuda_check(cudaMalloc(&plan->psi_tiled, sizeof(double) * pt), "cudaMalloc psi_tiled");
+      if (!rc) rc = cuda_check(cudaMemset(plan->psi_tiled, 0, sizeof(double) * pt), "memset");
+      std::vector<PadTask> tt;
+      for (int64_t i = 0; i < nk; ++i) {
+        const int m = d->dim_l[keys[i].jl], n = d->dim_r[keys[i].jr];
+        const int w = GemmBatch::col_tile_width(n);
+        for (int c0 = 0, ct = 0; c0 < n; c0 += w, ++ct)
+          tt.push_back({plan->offs[i] + c0, plan->ptoffs[i] + (int64_t)ct * pad16(m) * NC_LD_B, m,
+                        std::min(w, n - c0), n, NC_LD_B});
+      }
+      if (!rc) rc = upload_vec(tt, &plan->psit_copy.d_tasks);
+      plan->psit_copy.n = static_cast<int64_t>(tt.size());
+    }
   }
   if (!rc && !d->dry_run && getenv("SDMRG_SIDE_STREAM")) {
     int lo = 0, hi = 0;
@@ -917,7 +976,15 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     rc = cuda_check(cudaGetLastError(), "psi pad launch");
     if (rc) return rc;
   }
+  if (plan->psit_copy.n > 0) {
+    pad_kernel<<<static_cast<unsigned>(std::min<int64_t>(plan->psit_copy.n, 148 * 8)), 256, 0,
+                 stream>>>(plan->psit_copy.d_tasks, plan->psit_copy.n, psi, plan->psi_tiled);
+    count_launch();
+    rc = cuda_check(cudaGetLastError(), "psi tiled launch");
+    if (rc) return rc;
+  }
   Bases bases{};
+  bases.p[B_PSIT] = plan->psi_tiled;
   bases.p[B_PSI] = plan->psi_pad;
   bases.p[B_SIGMA] = sigma;
   bases.p[B_ARENA_L] = const_cast<double*>(plan->arena_l);
@@ -1011,6 +1078,8 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
   if (plan->arena_r) cudaFree(plan->arena_r);
   if (plan->psi_pad) cudaFree(plan->psi_pad);
   plan->psi_copy.release();
+  plan->psit_copy.release();
+  if (plan->psi_tiled) cudaFree(plan->psi_tiled);
   if (plan->fork) cudaEventDestroy(plan->fork);
   if (plan->join) cudaEventDestroy(plan->join);
   if (plan->side) cudaStreamDestroy(plan->side);

@@ -71,7 +71,8 @@ int GemmBatch::begin_prob(uint64_t c, int ldc, int m, int n, int beta) {
   return static_cast<int>(probs.size()) - 1;
 }
 
-void GemmBatch::add_seg(uint64_t a, int lda, uint64_t b, int ldb, int k, double scale) {
+void GemmBatch::add_seg(uint64_t a, int lda, uint64_t b, int ldb, int k, double scale,
+                        int btile) {
   if (k <= 0) return;  // the engine requires non-empty segments
   Seg s{};
   s.a = a;
@@ -79,9 +80,15 @@ void GemmBatch::add_seg(uint64_t a, int lda, uint64_t b, int ldb, int k, double 
   s.lda = lda;
   s.ldb = ldb;
   s.k = k;
+  s.btile = btile;
   s.scale = scale;
   segs.push_back(s);
   probs.back().seg_end = static_cast<int32_t>(segs.size());
+}
+
+int GemmBatch::col_tile_width(int n) {
+  const int nt = (n + BN - 1) / BN;
+  return std::max(((n + nt - 1) / nt + 7) / 8 * 8, 8);
 }
 
 void GemmBatch::end_prob() {
@@ -100,7 +107,7 @@ void GemmBatch::end_prob() {
   for (int r0 = 0; r0 < p.m; r0 += tm)
     for (int c0 = 0; c0 < p.n; c0 += tn) {
       const int mm = std::min(tm, p.m - r0), nn = std::min(tn, p.n - c0);
-      Tile t{pi, r0, c0, static_cast<int16_t>(mm), static_cast<int16_t>(nn)};
+      Tile t{pi, r0, c0, static_cast<int16_t>(mm), static_cast<int16_t>(nn), tn};
       tiles.push_back(t);
       tile_cost.push_back(double(ksum) * ((mm + 7) / 8 * 8) * ((nn + 7) / 8 * 8) + 4096.0);
     }
@@ -163,7 +170,8 @@ int GemmBatch::upload(DeviceBatch* out, cudaStream_t stream) const {
     for (size_t i = 0; i < tiles.size(); ++i) {
       const Tile& t = tiles[i];
       const Prob& p = probs[t.prob];
-      recs[i] = TileRec{p.c, p.ldc, p.beta, p.seg_begin, p.seg_end, t.row0, t.col0, t.tm, t.tn, 0};
+      recs[i] = TileRec{p.c, p.ldc, p.beta, p.seg_begin, p.seg_end, t.row0, t.col0, t.tm, t.tn,
+                        t.colw};
     }
     if ((rc = cuda_check(cudaMalloc(&out->tiles, recs.size() * sizeof(TileRec)), "cudaMalloc tiles")))
       return rc;

@@ -36,7 +36,9 @@ struct GemmBatch {
   int begin_prob(uint64_t c, int ldc, int m, int n, int beta);
   // move another batch's problems, segments and tiles behind this one's
   void append(GemmBatch&& other);
-  void add_seg(uint64_t a, int lda, uint64_t b, int ldb, int k, double scale);
+  void add_seg(uint64_t a, int lda, uint64_t b, int ldb, int k, double scale, int btile = 0);
+  // the column-tile width end_prob uses for an n-column problem
+  static int col_tile_width(int n);
   void end_prob();
   // order tiles by descending cost (longest-processing-time first)
   void finalize_tiles();
