@@ -7,8 +7,9 @@ reference's interfaces for that path:
 
   build_plan / apply_plan / DevicePlan   blocks.py:503, dmrg.py:107
   lanczos_ground                         dmrg.py:43
-  sbmm4s, CudaGemm                       sbmm4s.py:165, gemm.py:50
-  rotate_operators, rdm_blocks           dmrg.py:254, dmrg.py:221
+  sbmm4s, CudaGemm                       sbmm4s.py:167, gemm.py:53
+  renormalize_store, rotate_operators,   dmrg.py:335, dmrg.py:254,
+  reduced_density_matrix                 dmrg.py:221
 """
 
 __version__ = "0.1.0"
@@ -31,4 +32,8 @@ def __getattr__(name):
     if name in ("sbmm4s", "DeviceProblem", "flops_fused"):
         from . import sbmm4s
         return getattr(sbmm4s, name)
+    if name in ("renormalize_store", "renormalize_blocks", "rotate_operators",
+                "reduced_density_matrix", "rdm_eigensystem", "truncate"):
+        from . import renorm
+        return getattr(renorm, name)
     raise AttributeError(name)
