@@ -199,9 +199,13 @@ int sdmrg_plan_arena(const sdmrg_plan* plan, int side, double** base, int64_t* s
 /* Shard ownership: mine[i] = 1 when ψ key i is this rank's input sector
  * (psi_keys entries).  Every key belongs to exactly one rank of `world`.    */
 int sdmrg_plan_shard(const sdmrg_plan* plan, int32_t* mine);
-/* sigma (+)= H_eff psi over this rank's shard; device vectors of psi_size. */
+/* sigma (+)= H_eff psi over this rank's shard; device vectors of psi_size.
+ * The operator pre-sums (phase 0: ψ-independent) are formed by the first
+ * apply and reused by later ones; after changing the arenas in place call
+ * sdmrg_plan_invalidate so the next apply forms them again.                 */
 int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma,
                      int accumulate, void* stream);
+int sdmrg_plan_invalidate(sdmrg_plan* plan);
 /* Per-launch CUDA-event timing of subsequent applies (bench instrumentation).
  * sdmrg_plan_timing syncs the last apply's events and writes, per phase
  * (0: left-operator pre-summation, 1: T = A R^T, 2: σ += Lsum T, 3: split-K

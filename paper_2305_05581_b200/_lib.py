@@ -85,6 +85,7 @@ _SIGS = {
     "sdmrg_plan_arena": (c_int, [c_vp, c_int, ctypes.POINTER(c_vp), P_i64, P_i64]),
     "sdmrg_plan_apply": (c_int, [c_vp, c_vp, c_vp, c_int, c_vp]),
     "sdmrg_plan_destroy": (c_int, [c_vp]),
+    "sdmrg_plan_invalidate": (c_int, [c_vp]),
     "sdmrg_plan_set_timing": (c_int, [c_vp, c_int]),
     "sdmrg_plan_timing": (c_int, [c_vp, P_dbl, P_i64, P_i64]),
     "sdmrg_dot": (c_int, [c_i64, c_vp, c_vp, c_vp, c_vp]),

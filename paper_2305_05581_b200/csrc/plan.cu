@@ -41,7 +41,7 @@ namespace {
 // (even leading dimensions, even element offsets, zero pads): the operator
 // arenas (repacked once at build), ψ (copied per apply) and the workspace.
 // σ is only written (epilogue) and keeps the reference layout.
-enum { B_PSI = 0, B_SIGMA = 1, B_ARENA_L = 2, B_ARENA_R = 3, B_WS = 4, B_PSIT = 5 };
+enum { B_PSI = 0, B_SIGMA = 1, B_ARENA_L = 2, B_ARENA_R = 3, B_WS = 4, B_PSIT = 5, B_LSUM = 6 };
 
 // Stage-tiled T (phase 2's B operand): T(i, b) (m x r) is stored as column
 // tiles of the σ problems' width w = col_tile_width(r), each a contiguous
@@ -160,6 +160,13 @@ struct sdmrg_plan {
   std::vector<char> mine;          // ψ keys of this rank's shard
   PadList psi_copy;                // ψ -> psi_pad block list (device)
   PadList psit_copy;               // ψ -> psi_tiled (stage-tiled ψ, phase 2 B)
+  // Pre-summed left operators (phase 0) depend on the operators and the
+  // table only — not on ψ — so they live in their own buffer, computed by
+  // the first apply after the arenas are final and reused by every later
+  // apply of the plan (a Lanczos / Davidson loop)
+  double* lsum = nullptr;
+  int64_t lsum_doubles = 0;
+  bool lsum_ready = false;
   double* psi_tiled = nullptr;
   std::vector<int64_t> ptoffs;     // psi_tiled block offsets
   bool tiled = false;
@@ -501,7 +508,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     std::vector<int32_t> rops;
     for (const Pair& p : pairs[i]) {
       rops.push_back(p.rop);
-      if (p.term_end - p.term_begin > 1) t_need[i] += (int64_t)d->dim_l[keys[p.out].jl] * pad2(m);
+      (void)p;  // pre-summed left operators live in the persistent lsum buffer
     }
     std::sort(rops.begin(), rops.end());
     rops.erase(std::unique(rops.begin(), rops.end()), rops.end());
@@ -551,6 +558,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
 
   const int64_t taskgen_ms = ms_since(t_start);
   const auto t_emit = clk::now();
+  int64_t lsum_pos = 0;  // running offset in the persistent lsum buffer
   int64_t i0 = d->dry_run ? nk : 0;  // dry run: task generation + stats only
   while (i0 < nk) {
     Chunk ch;
@@ -693,16 +701,16 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
             sg.a = make_handle(B_ARENA_L, poff_l[(size_t)t.lop * nL + keys[i].jl]);
             sg.scale = t.coef;
           } else {
-            CombOut co{make_handle(B_WS, ws), static_cast<int32_t>(ch.comb0.terms.size()), 0};
+            CombOut co{make_handle(B_LSUM, lsum_pos), static_cast<int32_t>(ch.comb0.terms.size()), 0};
             for (int32_t x = pr.term_begin; x < pr.term_end; ++x)
               ch.comb0.terms.push_back(
                   {make_handle(B_ARENA_L, poff_l[(size_t)tt[x].lop * nL + keys[i].jl]),
                    tt[x].coef});
             co.term_end = static_cast<int32_t>(ch.comb0.terms.size());
             ch.comb0.outs.push_back(co);
-            sg.a = make_handle(B_WS, ws);
+            sg.a = make_handle(B_LSUM, lsum_pos);
             sg.scale = 1.0;
-            ws += qm;
+            lsum_pos += qm;
             ch.flops0 += 2LL * (co.term_end - co.term_begin) * qm;
             ch.bytes0 += 8LL * (co.term_end - co.term_begin + 1) * qm;
             ++comb_outputs;
@@ -776,6 +784,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     i0 = i1;
   }
 
+  plan->lsum_doubles = lsum_pos;
   const int64_t emit_ms = ms_since(t_emit);
   const auto t_dev = clk::now();
   int64_t ws_max = 0;
@@ -856,6 +865,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&plan->fork, cudaEventDisableTiming), "event");
     if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&plan->join, cudaEventDisableTiming), "event");
   }
+  if (!rc && plan->lsum_doubles > 0)
+    rc = cuda_check(cudaMalloc(&plan->lsum, sizeof(double) * plan->lsum_doubles), "cudaMalloc lsum");
   if (!rc && ws_max > 0) {
     rc = cuda_check(cudaMalloc(&plan->workspace, sizeof(double) * ws_max), "cudaMalloc workspace");
     // T pads are never written by the engine: zero them once
@@ -984,6 +995,7 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (rc) return rc;
   }
   Bases bases{};
+  bases.p[B_LSUM] = plan->lsum;
   bases.p[B_PSIT] = plan->psi_tiled;
   bases.p[B_PSI] = plan->psi_pad;
   bases.p[B_SIGMA] = sigma;
@@ -1001,8 +1013,10 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
       cudaStreamWaitEvent(plan->side, plan->fork, 0);
     }
     if (plan->timing) cudaEventRecord(ch.ev[0], s0);
-    rc = launch_combine(ch.comb0, bases, s0);
-    if (rc) return rc;
+    if (!plan->lsum_ready) {
+      rc = launch_combine(ch.comb0, bases, s0);
+      if (rc) return rc;
+    }
     if (plan->timing) cudaEventRecord(ch.ev[1], s0);
     if (fork) cudaEventRecord(plan->join, plan->side);
     if (plan->timing) cudaEventRecord(ch.ev[2], stream);
@@ -1021,6 +1035,13 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (rc) return rc;
     if (plan->timing) cudaEventRecord(ch.ev[7], stream);
   }
+  plan->lsum_ready = true;
+  return SDMRG_OK;
+}
+
+int sdmrg_plan_invalidate(sdmrg_plan* plan) {
+  if (!plan) return fail(SDMRG_EINVAL, "plan_invalidate: null plan");
+  plan->lsum_ready = false;
   return SDMRG_OK;
 }
 
@@ -1074,6 +1095,7 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
       if (e) cudaEventDestroy(e);
   }
   if (plan->workspace) cudaFree(plan->workspace);
+  if (plan->lsum) cudaFree(plan->lsum);
   if (plan->arena_l) cudaFree(plan->arena_l);
   if (plan->arena_r) cudaFree(plan->arena_r);
   if (plan->psi_pad) cudaFree(plan->psi_pad);

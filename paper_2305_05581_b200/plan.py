@@ -206,6 +206,11 @@ class DevicePlan:
 
     __call__ = apply
 
+    def invalidate(self):
+        """The arenas changed in place: the next apply re-forms the operator
+        pre-sums (sdmrg_plan_invalidate)."""
+        _lib.check(_lib.load().sdmrg_plan_invalidate(self._h))
+
     def set_timing(self, enable=True):
         """Record CUDA events around every engine launch of later applies."""
         _lib.check(_lib.load().sdmrg_plan_set_timing(self._h, int(bool(enable))))

@@ -181,6 +181,7 @@ def fill_plan_arenas(plan, pi, seed=0):
                 blk.zero_()
                 blk[:, :n].fill_diagonal_(1.0)
     torch.cuda.synchronize()
+    plan.invalidate()  # operator pre-sums (if any) follow the new arenas
 
 
 def _rows_of(pi, side, op, j):
