@@ -162,7 +162,9 @@ class DevicePlan:
 
     def padded_arena(self, side):
         """(CUDA tensor view of the plan-owned padded arena, offsets[nops, nsec])
-        for side 'l' or 'r' (sdmrg_plan_arena)."""
+        for side 'l' or 'r' (sdmrg_plan_arena).  The view aliases plan memory:
+        valid only while the plan lives; call ``invalidate()`` after writing
+        through it once the plan has been applied."""
         k = {"l": 0, "r": 1}[side]
         nops = self.pi.kind_l.shape[0] if k == 0 else self.pi.kind_r.shape[0]
         nsec = self.pi.dim_l.shape[0] if k == 0 else self.pi.dim_r.shape[0]
