@@ -202,7 +202,10 @@ def test_device_lanczos_dense_problems():
 def test_dgemm_all_layouts(ta, tb):
     from paper_2305_05581_b200 import _lib
     rng = np.random.default_rng(ta * 2 + tb)
-    for m, n, k in ((1, 1, 1), (7, 5, 3), (64, 64, 16), (65, 130, 33), (200, 17, 301), (8, 8, 0)):
+    # even extents take the 16-byte (aligned) load path, odd ones the 8-byte
+    # path; k tails of 1..15 exercise the zero-filled pairs
+    for m, n, k in ((1, 1, 1), (7, 5, 3), (64, 64, 16), (65, 130, 33), (200, 17, 301), (8, 8, 0),
+                    (96, 128, 37), (130, 66, 2), (64, 200, 129), (2, 2, 17)):
         a = rng.standard_normal((k, m) if ta else (m, k))
         b = rng.standard_normal((n, k) if tb else (k, n))
         c0 = rng.standard_normal((m, n))
