@@ -167,6 +167,7 @@ struct sdmrg_plan {
   double* lsum = nullptr;
   int64_t lsum_doubles = 0;
   bool lsum_ready = false;
+  bool lsum_persistent = true;     // false: pre-sums in the chunk workspace, per apply
   double* psi_tiled = nullptr;
   std::vector<int64_t> ptoffs;     // psi_tiled block offsets
   bool tiled = false;
@@ -501,14 +502,14 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
 
   // ---- execution schedule: chunks of ψ keys bounded by the workspace
   // (distinct non-identity T blocks + pre-summed left operators per key)
-  std::vector<int64_t> t_need(nk, 0);
+  std::vector<int64_t> t_need(nk, 0), l_need(nk, 0);
   for (int64_t i = 0; i < nk; ++i) {
     if (!mine[i]) continue;
     const int64_t m = d->dim_l[keys[i].jl];
     std::vector<int32_t> rops;
     for (const Pair& p : pairs[i]) {
       rops.push_back(p.rop);
-      (void)p;  // pre-summed left operators live in the persistent lsum buffer
+      if (p.term_end - p.term_begin > 1) l_need[i] += (int64_t)d->dim_l[keys[p.out].jl] * pad2(m);
     }
     std::sort(rops.begin(), rops.end());
     rops.erase(std::unique(rops.begin(), rops.end()), rops.end());
@@ -518,13 +519,23 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       t_need[i] += plan->tiled ? tiled_size((int)m, d->dim_r[jrp]) : m * pad2(d->dim_r[jrp]);
     }
   }
+  // Pre-sums persist across applies (formed once) when they take at most a
+  // quarter of free HBM; otherwise they live in the chunk workspace and are
+  // re-formed by every apply (large D), as the workspace is reused per chunk.
+  int64_t total_l = 0;
+  for (int64_t i = 0; i < nk; ++i) total_l += l_need[i];
+  size_t free_b = 0, total_b = 0;
+  if (!d->dry_run) cudaMemGetInfo(&free_b, &total_b);
+  plan->lsum_persistent =
+      !d->dry_run && (double)total_l * 8.0 <= 0.25 * (double)free_b && !getenv("SDMRG_LSUM_PER_APPLY");
+  if (!plan->lsum_persistent)
+    for (int64_t i = 0; i < nk; ++i) t_need[i] += l_need[i];
   int64_t total_t = 0;
   for (int64_t i = 0; i < nk; ++i) total_t += t_need[i];
   int64_t budget = d->workspace_doubles;
   if (budget <= 0 && !d->dry_run) {
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    budget = std::max<int64_t>(1 << 20, (int64_t)(free_b / 8 * 0.30));
+    const double avail = (double)free_b - (plan->lsum_persistent ? 8.0 * total_l : 0.0);
+    budget = std::max<int64_t>(1 << 20, (int64_t)(avail / 8 * 0.30));
   }
   int64_t max_key = 0;
   for (int64_t i = 0; i < nk; ++i) max_key = std::max(max_key, t_need[i]);
@@ -701,16 +712,19 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
             sg.a = make_handle(B_ARENA_L, poff_l[(size_t)t.lop * nL + keys[i].jl]);
             sg.scale = t.coef;
           } else {
-            CombOut co{make_handle(B_LSUM, lsum_pos), static_cast<int32_t>(ch.comb0.terms.size()), 0};
+            const uint64_t lh = plan->lsum_persistent ? make_handle(B_LSUM, lsum_pos)
+                                                      : make_handle(B_WS, ws);
+            CombOut co{lh, static_cast<int32_t>(ch.comb0.terms.size()), 0};
             for (int32_t x = pr.term_begin; x < pr.term_end; ++x)
               ch.comb0.terms.push_back(
                   {make_handle(B_ARENA_L, poff_l[(size_t)tt[x].lop * nL + keys[i].jl]),
                    tt[x].coef});
             co.term_end = static_cast<int32_t>(ch.comb0.terms.size());
             ch.comb0.outs.push_back(co);
-            sg.a = make_handle(B_LSUM, lsum_pos);
+            sg.a = lh;
             sg.scale = 1.0;
-            lsum_pos += qm;
+            if (plan->lsum_persistent) lsum_pos += qm;
+            else ws += qm;
             ch.flops0 += 2LL * (co.term_end - co.term_begin) * qm;
             ch.bytes0 += 8LL * (co.term_end - co.term_begin + 1) * qm;
             ++comb_outputs;
@@ -1013,7 +1027,7 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
       cudaStreamWaitEvent(plan->side, plan->fork, 0);
     }
     if (plan->timing) cudaEventRecord(ch.ev[0], s0);
-    if (!plan->lsum_ready) {
+    if (!plan->lsum_ready || !plan->lsum_persistent) {
       rc = launch_combine(ch.comb0, bases, s0);
       if (rc) return rc;
     }
