@@ -120,6 +120,19 @@ struct Seg {         // 40 B
 #ifndef SDMRG_STCS
 #define SDMRG_STCS 0
 #endif
+// per-tile warp grid: 1 x 4 or 4 x 1 instead of 2 x 2 when a tile has an odd
+// number of 8-row (8-column) blocks, so the four DMMA warps stay balanced
+#ifndef SDMRG_GRID_ADAPT
+#define SDMRG_GRID_ADAPT 1
+#endif
+__host__ __device__ constexpr int cw_index(int wr, int wc) { return wr * 2 + wc; }
+// only for the T = A R^T instances (phase 1): in the phase-2 instance the extra
+// bodies push the consumer past its 96-register budget (spills; measured
+// slower at L=50 D=4096, profiles/r1_notes.md)
+template <bool TB>
+__host__ __device__ constexpr bool grid_adapt() {
+  return SDMRG_GRID_ADAPT && SDMRG_TILE == 64 && TB;
+}
 // K order inside a stage (same for both operands, so any bijection is
 // exact): DMMA k4 step ks, thread column lc reads stage k
 //   kperm(ks, lc) = 8 (ks >> 1) + 2 lc + (ks & 1)
@@ -475,6 +488,16 @@ __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring&
                                                  uint32_t& phase, uint32_t a_off, uint32_t b_off,
                                                  double* c, int ldc, int beta, int row_lim,
                                                  int col_lim, int lane) {
+  if constexpr (grid_adapt<TB>()) {
+    if (mblk > 4 || nblk > 4) {  // 1 x 4 / 4 x 1 warp grids of odd-block tiles
+      switch (mblk * 8 + nblk) {
+        SDMRG_TILE_CASE(7, 2) SDMRG_TILE_CASE(7, 1) SDMRG_TILE_CASE(5, 2) SDMRG_TILE_CASE(5, 1)
+        SDMRG_TILE_CASE(2, 7) SDMRG_TILE_CASE(1, 7) SDMRG_TILE_CASE(2, 5) SDMRG_TILE_CASE(1, 5)
+        default: break;
+      }
+      return;
+    }
+  }
   switch (mblk * 8 + nblk) {
 #if SDMRG_TILE > 64
     SDMRG_TILE_CASE(6, 6) SDMRG_TILE_CASE(6, 5) SDMRG_TILE_CASE(5, 6) SDMRG_TILE_CASE(5, 5)
@@ -834,13 +857,28 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
     // first stage of a tile: balanced 2 x 2 warp split of its 8x8 blocks
     const int tm = m.tm, tn = m.tn;
     const int mb = (tm + 7) >> 3, nb = (tn + 7) >> 3;
-    const int mb0 = (mb + 1) >> 1;
-    const int mblk = wr == 0 ? mb0 : mb - mb0;
-    const int wr0 = wr == 0 ? 0 : mb0 * 8;
-    // columns: balanced over WGRID_C warps
-    const int nbase = nb / WGRID_C, nextra = nb - nbase * WGRID_C;
-    const int nblk = nbase + (wc < nextra ? 1 : 0);
-    const int wc0 = 8 * (wc * nbase + min(wc, nextra));
+    int mblk, nblk, wr0, wc0;
+    if (grid_adapt<TB>() && CONSUMERS == 4 && (mb & 1) && (nb & 3) == 0 && mb <= 8 && nb <= 8) {
+      // odd block rows: a 2 x 2 split would give 4:3 row blocks; four warps
+      // side by side over all rows balance exactly (1 x 4 grid)
+      mblk = mb;
+      wr0 = 0;
+      nblk = nb >> 2;
+      wc0 = 8 * nblk * cw_index(wr, wc);
+    } else if (grid_adapt<TB>() && CONSUMERS == 4 && (nb & 1) && (mb & 3) == 0 && nb <= 8 && mb <= 8) {
+      nblk = nb;  // odd block columns: 4 x 1 grid
+      wc0 = 0;
+      mblk = mb >> 2;
+      wr0 = 8 * mblk * cw_index(wr, wc);
+    } else {
+      const int mb0 = (mb + 1) >> 1;
+      mblk = wr == 0 ? mb0 : mb - mb0;
+      wr0 = wr == 0 ? 0 : mb0 * 8;
+      // columns: balanced over WGRID_C warps
+      const int nbase = nb / WGRID_C, nextra = nb - nbase * WGRID_C;
+      nblk = nbase + (wc < nextra ? 1 : 0);
+      wc0 = 8 * (wc * nbase + min(wc, nextra));
+    }
     // fragment origin: stage k = lc (natural order) or 2 lc (kperm)
     const int kf = SDMRG_LDS128 ? 2 * lc : lc;
     const uint32_t a_off = TA ? (kf * NC_LD_A + wr0 + lr) * 8 : ((wr0 + lr) * KC_LD + kf) * 8;

@@ -171,6 +171,7 @@ struct sdmrg_plan {
   double* psi_tiled = nullptr;
   std::vector<int64_t> ptoffs;     // psi_tiled block offsets
   bool tiled = false;
+  bool stack_t = false;  // phase 1 per run of arena-adjacent right operators
   // optional (SDMRG_SIDE_STREAM=1): phase 0 (combine) on a low-priority side
   // stream concurrently with phase 1 (it only needs the L arena).  Measured
   // no gain at L=30 D=2048 (99.0 vs 99.4 ms, same box), and it blurs the
@@ -340,12 +341,14 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     plan->ptoffs[i + 1] =
         plan->ptoffs[i] + tiled_size(d->dim_l[keys[i].jl], d->dim_r[keys[i].jr]);
   // padded arena offsets: block (op, column sector j) has rows dim(j + delta),
-  // row stride pad2(dim(j))
+  // row stride pad2(dim(j)); right-arena blocks also get an even row count
+  // (one pad row when dim(j + delta) is odd) so that a run of adjacent right
+  // blocks is one matrix whose T = A R^T columns start at even offsets
   // column-sector-major: all operators' blocks of column sector j are one
   // contiguous run of rows with the same row stride pad2(dim(j)) (the R
   // blocks a ψ key's phase 1 reads sit together; fillers see 2-d runs)
   auto pad_offsets = [](int nops, int nsec, const int64_t* boff, const int32_t* shift,
-                        const int32_t* dim, std::vector<int64_t>& out) {
+                        const int32_t* dim, bool even_rows, std::vector<int64_t>& out) {
     out.assign((size_t)nops * nsec, -1);
     int64_t pos = 0;
     for (int j = 0; j < nsec; ++j)
@@ -353,7 +356,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
         const size_t x = (size_t)o * nsec + j;
         if (boff[x] < 0 || shift[x] < 0) continue;
         out[x] = pos;
-        pos += (int64_t)dim[shift[x]] * pad2(dim[j]);
+        pos += (int64_t)(even_rows ? pad2(dim[shift[x]]) : dim[shift[x]]) * pad2(dim[j]);
       }
     return pos;
   };
@@ -361,8 +364,9 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   const std::vector<int32_t> shL = shift_table(d->nops_l, d->delta_l, nL, d->qn_l, nc);
   const std::vector<int32_t> shR = shift_table(d->nops_r, d->delta_r, nR, d->qn_r, nc);
   std::vector<int64_t> poff_l, poff_r;
-  const int64_t psize_l = pad_offsets(d->nops_l, nL, d->blk_off_l, shL.data(), d->dim_l, poff_l);
-  const int64_t psize_r = pad_offsets(d->nops_r, nR, d->blk_off_r, shR.data(), d->dim_r, poff_r);
+  const int64_t psize_l = pad_offsets(d->nops_l, nL, d->blk_off_l, shL.data(), d->dim_l, false, poff_l);
+  const int64_t psize_r = pad_offsets(d->nops_r, nR, d->blk_off_r, shR.data(), d->dim_r, true, poff_r);
+  plan->stack_t = !plan->tiled && getenv("SDMRG_NO_STACK_T") == nullptr;
 
   // ---- task generation: members per ψ key, rows in table order
   std::vector<std::vector<Member>> per_key(nk);
@@ -585,6 +589,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       int32_t ld;
       uint64_t handle;
       int32_t btile;  // > 0: stage-tiled T (phase 2 B operand)
+      int32_t run;    // > 0: first of `run` arena-adjacent right ops (one product)
     };
     std::vector<std::vector<TEntry>> tmap(i1 - i0);
     auto t_lookup = [&](int64_t i, int32_t ro) -> const TEntry& {
@@ -612,18 +617,49 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       for (const int32_t ro : rops) {
         if (d->kind_r[ro] == 1) {  // R = identity: T = A (no product)
           if (plan->tiled)
-            tm.push_back({ro, NC_LD_B, make_handle(B_PSIT, plan->ptoffs[i]), pad16(m)});
+            tm.push_back({ro, NC_LD_B, make_handle(B_PSIT, plan->ptoffs[i]), pad16(m), 0});
           else
-            tm.push_back({ro, pad2(n), make_handle(B_PSI, plan->poffs[i]), 0});
+            tm.push_back({ro, pad2(n), make_handle(B_PSI, plan->poffs[i]), 0, 0});
           continue;
         }
         const int r = d->dim_r[shR[(size_t)ro * nR + k.jr]];
         if (plan->tiled) {
-          tm.push_back({ro, NC_LD_B, make_handle(B_WS, need), pad16(m)});  // rebased below
+          tm.push_back({ro, NC_LD_B, make_handle(B_WS, need), pad16(m), 1});  // rebased below
           need += tiled_size(m, r);
         } else {
-          tm.push_back({ro, pad2(r), make_handle(B_WS, need), 0});  // relative; rebased below
+          tm.push_back({ro, pad2(r), make_handle(B_WS, need), 0, 1});  // relative; rebased below
           need += (int64_t)m * pad2(r);
+        }
+      }
+      // Right ops whose arena blocks are adjacent (column-sector-major arena,
+      // even row counts) form one stacked matrix [R_b1; R_b2; ...] with row
+      // stride pad2(n): T for the whole run is ONE m x sum(pad2(r_b)) product
+      // with T(i, b) its column block (ld = the run width).  Fewer, fuller
+      // 64 x 64 tiles than one product per operator (L=30 D=2048: 2.62 M ->
+      // 1.63 M phase-1 tiles, tools/stack_stats.py).  Same workspace size.
+      if (plan->stack_t) {
+        int64_t pos = 0;  // relative workspace position of the run being formed
+        for (size_t u = 0; u < tm.size();) {
+          if (d->kind_r[tm[u].rop] == 1) { ++u; continue; }
+          size_t v = u + 1;
+          int64_t end = poff_r[(size_t)tm[u].rop * nR + k.jr] + (int64_t)tm[u].ld * pad2(n);
+          int width = tm[u].ld;
+          while (v < tm.size() && d->kind_r[tm[v].rop] != 1 &&
+                 poff_r[(size_t)tm[v].rop * nR + k.jr] == end) {
+            end += (int64_t)tm[v].ld * pad2(n);
+            width += tm[v].ld;
+            ++v;
+          }
+          int col = 0;
+          for (size_t x = u; x < v; ++x) {
+            const int w = tm[x].ld;
+            tm[x].handle = make_handle(B_WS, pos + col);
+            tm[x].ld = width;
+            tm[x].run = x == u ? static_cast<int32_t>(v - u) : 0;
+            col += w;
+          }
+          pos += (int64_t)m * width;
+          u = v;
         }
       }
       ws_key[i - i0 + 1] = need;
@@ -637,13 +673,23 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       const Key& k = keys[i];
       const int m = d->dim_l[k.jl], n = d->dim_r[k.jr];
       GemmBatch& gb = p1key[i - i0];
-      for (TEntry& te : tmap[i - i0]) {
+      auto& tv = tmap[i - i0];
+      for (size_t x = 0; x < tv.size(); ++x) {
+        TEntry& te = tv[x];
         if (d->kind_r[te.rop] == 1) continue;
         const int64_t base = ws_key[i - i0] + (int64_t)(te.handle & kHandleMask);
         te.handle = make_handle(B_WS, base);
         const int r = d->dim_r[shR[(size_t)te.rop * nR + k.jr]];
         const uint64_t rblk = make_handle(B_ARENA_R, poff_r[(size_t)te.rop * nR + k.jr]);
-        if (te.btile > 0) {
+        f1 += 2LL * m * n * r;
+        ++np1;
+        if (te.run == 0) continue;  // inside a stacked run: formed by its first op
+        if (plan->stack_t) {
+          // te.ld = run width: T(run) = A [R_b ...]^T, m x width
+          gb.begin_prob(te.handle, te.ld, m, te.ld, 0);
+          gb.add_seg(make_handle(B_PSI, plan->poffs[i]), pad2(n), rblk, pad2(n), n, 1.0);
+          gb.end_prob();
+        } else if (te.btile > 0) {
           // one problem per column tile of T, written as its [pad16(m)][NC_LD_B] block
           const int w = GemmBatch::col_tile_width(r);
           for (int c0 = 0, ct = 0; c0 < r; c0 += w, ++ct) {
@@ -658,8 +704,6 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
           gb.add_seg(make_handle(B_PSI, plan->poffs[i]), pad2(n), rblk, pad2(n), n, 1.0);
           gb.end_prob();
         }
-        f1 += 2LL * m * n * r;
-        ++np1;
       }
     }
     for (auto& gb : p1key) ch.host1.append(std::move(gb));
