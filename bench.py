@@ -245,7 +245,10 @@ def scale_point(n_orb, d, seed, peak, applies=3, n_elec=None):
            "D": d, "ms_per_step": best, "ref_tflops": st["ref_flops"] / (best * 1e-3) / 1e12,
            "exec_tflops": st["exec_flops"] / (best * 1e-3) / 1e12,
            "exec_frac_of_dgemm": (st["exec_flops"] / (best * 1e-3) / 1e12) / peak if peak else None,
-           "chunks": st["chunks"], "psi_size": st["psi_size"]}
+           "chunks": st["chunks"], "psi_size": st["psi_size"],
+           "worklist": {"products": st["products"], "t_problems": st["t_problems"],
+                        "tiles": st["tiles"], "segments": st["segments"],
+                        "exec_mflop_per_tile": st["exec_flops"] / max(st["tiles"], 1) / 1e6}}
     plan.close()
     del plan, psi, out
     torch.cuda.empty_cache()

@@ -129,6 +129,13 @@ __host__ __device__ constexpr int cw_index(int wr, int wc) { return wr * 2 + wc;
 // only for the T = A R^T instances (phase 1): in the phase-2 instance the extra
 // bodies push the consumer past its 96-register budget (spills; measured
 // slower at L=50 D=4096, profiles/r1_notes.md)
+// Phase 2 alternates scaled single-operator segments with unit-scale
+// pre-summed ones inside one tile, so both consumer bodies of a tile shape are
+// hot.  With many distinct tile shapes (small sectors) that overflows the
+// instruction cache (ncu, L=50 D=4096: 24% of phase-2 stall samples were
+// no_instruction); the ONE instance runs a single always-scaling body instead
+// (a DMUL per fragment, a few % of the FP64 pipe).  The plan picks it per
+// launch from its tile-shape mix (plan.cu).
 template <bool TB>
 __host__ __device__ constexpr bool grid_adapt() {
   return SDMRG_GRID_ADAPT && SDMRG_TILE == 64 && TB;
@@ -274,7 +281,7 @@ struct Ring {
 // A warp owning MB x NB 8x8 blocks of a tile: runs every stage of the tile
 // (the first one already waited for), then the epilogue.  a_off/b_off: byte
 // offset of fragment (block 0, k4 step 0) within a stage.
-template <bool TA, bool TB, int MB, int NB>
+template <bool TA, bool TB, int MB, int NB, bool ONE>
 __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint32_t& phase,
                                              uint32_t a_off, uint32_t b_off, double* c, int ldc,
                                              int beta, int row_lim, int col_lim, int lane) {
@@ -420,8 +427,12 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
         }
 #endif
       };
-      if (scaled) body(std::true_type{});
-      else body(std::false_type{});
+      if constexpr (ONE) {
+        body(std::true_type{});  // unit scales multiply too: half the code
+      } else {
+        if (scaled) body(std::true_type{});
+        else body(std::false_type{});
+      }
     }
 #endif
     __syncwarp();
@@ -479,11 +490,12 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
 
 #define SDMRG_TILE_CASE(MB, NB)                                                                   \
   case (MB) * 8 + (NB):                                                                           \
-    consume_tile<TA, TB, MB, NB>(ring, stage, phase, a_off, b_off, c, ldc, beta, row_lim, col_lim, \
-                                 lane);                                                           \
+    consume_tile<TA, TB, MB, NB, ONE>(ring, stage, phase, a_off, b_off, c, ldc, beta, row_lim,      \
+                                      col_lim,                                                \
+                                      lane);                                                  \
     break;
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, bool ONE>
 __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring& ring, int& stage,
                                                  uint32_t& phase, uint32_t a_off, uint32_t b_off,
                                                  double* c, int ldc, int beta, int row_lim,
@@ -511,7 +523,7 @@ __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring&
     SDMRG_TILE_CASE(2, 4) SDMRG_TILE_CASE(2, 3) SDMRG_TILE_CASE(2, 2) SDMRG_TILE_CASE(2, 1)
     SDMRG_TILE_CASE(1, 4) SDMRG_TILE_CASE(1, 3) SDMRG_TILE_CASE(1, 2) SDMRG_TILE_CASE(1, 1)
     default:  // no blocks for this warp: walk the tile's stages
-      consume_tile<TA, TB, 0, 0>(ring, stage, phase, a_off, b_off, c, ldc, beta, row_lim, col_lim,
+      consume_tile<TA, TB, 0, 0, ONE>(ring, stage, phase, a_off, b_off, c, ldc, beta, row_lim, col_lim,
                                  lane);
       break;
   }
@@ -810,7 +822,8 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
 #else
 #define SDMRG_KERNEL_BOUNDS __launch_bounds__(THREADS, SDMRG_MINB)
 #endif
-template <bool TA, bool TB, bool BULK>
+// ONE: single always-scaling consumer body (see one_body_default)
+template <bool TA, bool TB, bool BULK, bool ONE = false>
 __global__ void SDMRG_KERNEL_BOUNDS
 seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __restrict__ segs,
                 int* __restrict__ counter, Bases bases) {
@@ -885,7 +898,7 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
     const uint32_t b_off =
         A_EL * 8 + (TB ? ((wc0 + lr) * KC_LD + kf) * 8 : (kf * NC_LD_B + wc0 + lr) * 8);
     double* c = m.c + (int64_t)(wr0 + lr) * m.ldc + wc0 + 2 * lc;
-    consume_dispatch<TA, TB>(mblk, nblk, ring, stage, phase, a_off, b_off, c, m.ldc, m.beta,
+    consume_dispatch<TA, TB, ONE>(mblk, nblk, ring, stage, phase, a_off, b_off, c, m.ldc, m.beta,
                              tm - wr0 - lr, tn - wc0 - 2 * lc, lane);
   }
 }

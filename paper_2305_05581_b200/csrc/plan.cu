@@ -134,6 +134,7 @@ struct Chunk {
   int64_t ws_doubles = 0;
   int64_t flops0 = 0, flops1 = 0, flops2 = 0;
   int64_t bytes0 = 0, bytes3 = 0;
+  bool p2_one_body = false;  // phase 2 on the single-body engine instance
   cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
@@ -248,6 +249,25 @@ int upload_vec(const std::vector<T>& v, T** out) {
 
 // Split-K granule = 1/split_factor of one persistent CTA's share of the
 // phase-2 work (SDMRG_SPLIT overrides; experiments).
+// Phase-2 engine instance: the single-body one when less than half of the
+// work sits in full 8 x 8-block tiles (every warp on the 4 x 4 body): a wide
+// tile-shape mix is what overflows the instruction cache.  L=30 D=2048 (56%
+// full) keeps two bodies (1.3 ms faster); L=50 D=4096 (40%) takes one
+// (6 ms faster, profiles/r1_notes.md).  SDMRG_ONE_BODY=0/1 forces it.
+bool use_one_body(const GemmBatch& gb) {
+  const char* env = getenv("SDMRG_ONE_BODY");
+  if (env) return atoi(env) != 0;
+  double full = 0.0, all = 0.0;
+  for (size_t t = 0; t < gb.tiles.size(); ++t) {
+    all += gb.tile_cost[t];
+    if (gb.tiles[t].tm > 56 && gb.tiles[t].tn > 56) full += gb.tile_cost[t];
+  }
+  return all > 0.0 && full < 0.5 * all;
+}
+int p2_octaves() {
+  static const int v = getenv("SDMRG_P2_OCTAVES") ? atoi(getenv("SDMRG_P2_OCTAVES")) : 0;
+  return v;
+}
 double split_factor() {
   const char* e = getenv("SDMRG_SPLIT");
   return e ? std::max(1.0, atof(e)) : 96.0;
@@ -784,6 +804,10 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       }
       outs.push_back(std::move(op));
     }
+    if (p2_octaves() > 0)  // σ blocks sharing T(i, b) share the right sector
+      std::stable_sort(outs.begin(), outs.end(), [&](const OutProb& a, const OutProb& b) {
+        return keys[a.o].jr < keys[b.o].jr;
+      });
     // split-K for load balance: a σ tile whose K work exceeds the granule
     // (1/96 of one persistent CTA's share: short tiles keep sibling tiles of one
     // σ block in step, so their shared operand panels hit in L2 — 1/6 was 5%
@@ -834,7 +858,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       ch.bytes3 += 8LL * (co.term_end - co.term_begin + 1) * qr;
     }
     ch.host1.finalize_tiles();
-    ch.host2.finalize_tiles();
+    ch.host2.finalize_tiles(p2_octaves());
+    ch.p2_one_body = use_one_body(ch.host2);
     ch.ws_doubles = ws;
     tiles += (int64_t)(ch.host1.tiles.size() + ch.host2.tiles.size());
     segments += (int64_t)(ch.host1.segs.size() + ch.host2.segs.size());
@@ -1083,7 +1108,8 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (plan->timing) cudaEventRecord(ch.ev[3], stream);
     if (fork) cudaStreamWaitEvent(stream, plan->join, 0);
     if (plan->timing) cudaEventRecord(ch.ev[4], stream);
-    rc = launch_engine(false, false, ch.p2, bases, plan->counters + 2 * c + 1, stream, true);
+    rc = launch_engine(false, false, ch.p2, bases, plan->counters + 2 * c + 1, stream, true,
+                       ch.p2_one_body);
     if (rc) return rc;
     if (plan->timing) {
       cudaEventRecord(ch.ev[5], stream);

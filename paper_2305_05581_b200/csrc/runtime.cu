@@ -1,3 +1,4 @@
+#include <cmath>
 // runtime.cu — engine launch plumbing and the GEMM-level C-ABI entry points
 // (gemm.py backend contract and sbmm4s.py Alg. 2).
 #include <algorithm>
@@ -37,6 +38,9 @@ static int grid_for() {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<TA, TB>());
     cudaFuncSetAttribute(seg_gemm_kernel<TA, TB, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<TA, TB>());
+    if (!TA && !TB)
+      cudaFuncSetAttribute(seg_gemm_kernel<false, false, true, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<TA, TB>());
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, seg_gemm_kernel<TA, TB, true>, THREADS,
                                                   smem_bytes<TA, TB>());
     grid = sms * std::max(per, 1);
@@ -130,9 +134,11 @@ void GemmBatch::append(GemmBatch&& o) {
   o = GemmBatch();
 }
 
-void GemmBatch::finalize_tiles() {
+void GemmBatch::finalize_tiles(int octaves) {
   // stable descending-cost order by bucketing on the (few) distinct costs:
   // O(n + u log u) instead of a comparison sort of millions of tiles
+  if (octaves > 0)
+    for (double& c : tile_cost) c = std::exp2(std::floor(std::log2(c) * octaves) / octaves);
   std::vector<double> uniq(tile_cost);
   std::sort(uniq.begin(), uniq.end(), std::greater<double>());
   uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
@@ -196,9 +202,16 @@ int GemmBatch::upload(DeviceBatch* out, cudaStream_t stream) const {
 }
 
 template <bool TA, bool TB>
-static void launch_t(bool bulk, const DeviceBatch& b, const Bases& bases, int* counter,
+static void launch_t(bool bulk, bool one, const DeviceBatch& b, const Bases& bases, int* counter,
                      cudaStream_t stream) {
   const int grid = std::min<int64_t>(grid_for<TA, TB>(), std::max<int64_t>(b.ntiles, 1));
+  if constexpr (!TA && !TB) {
+    if (bulk && one) {
+      seg_gemm_kernel<false, false, true, true><<<grid, THREADS, smem_bytes<TA, TB>(), stream>>>(
+          b.tiles, static_cast<int>(b.ntiles), b.segs, counter, bases);
+      return;
+    }
+  }
   if (bulk)
     seg_gemm_kernel<TA, TB, true><<<grid, THREADS, smem_bytes<TA, TB>(), stream>>>(
         b.tiles, static_cast<int>(b.ntiles), b.segs, counter, bases);
@@ -208,12 +221,12 @@ static void launch_t(bool bulk, const DeviceBatch& b, const Bases& bases, int* c
 }
 
 int launch_engine(bool ta, bool tb, const DeviceBatch& b, const Bases& bases, int* counter,
-                  cudaStream_t stream, bool bulk) {
+                  cudaStream_t stream, bool bulk, bool one_body) {
   if (b.ntiles == 0) return SDMRG_OK;
-  if (!ta && !tb) launch_t<false, false>(bulk, b, bases, counter, stream);
-  else if (!ta && tb) launch_t<false, true>(bulk, b, bases, counter, stream);
-  else if (ta && !tb) launch_t<true, false>(bulk, b, bases, counter, stream);
-  else launch_t<true, true>(bulk, b, bases, counter, stream);
+  if (!ta && !tb) launch_t<false, false>(bulk, one_body, b, bases, counter, stream);
+  else if (!ta && tb) launch_t<false, true>(bulk, false, b, bases, counter, stream);
+  else if (ta && !tb) launch_t<true, false>(bulk, false, b, bases, counter, stream);
+  else launch_t<true, true>(bulk, false, b, bases, counter, stream);
   count_launch();
   return cuda_check(cudaGetLastError(), "seg_gemm_kernel launch");
 }

@@ -41,7 +41,9 @@ struct GemmBatch {
   static int col_tile_width(int n);
   void end_prob();
   // order tiles by descending cost (longest-processing-time first)
-  void finalize_tiles();
+  // octaves > 0: costs bucketed to 1/octaves of a power of two (emission
+  // order kept inside a bucket) instead of exact distinct costs
+  void finalize_tiles(int octaves = 0);
   int upload(DeviceBatch* out, cudaStream_t stream) const;
   int64_t flops() const;  // useful (unpadded) FLOPs
 };
@@ -50,7 +52,8 @@ struct GemmBatch {
 // zeroed device int (reset by the caller or by this function when reset=1).
 // bulk: every operand row 16-byte aligned, even leading dimensions, zero
 // pads (engine.cuh BULK) — the H_eff plan's padded layouts only.
+// one_body: (!ta && !tb && bulk only) the single always-scaling consumer body
 int launch_engine(bool ta, bool tb, const DeviceBatch& b, const Bases& bases, int* counter,
-                  cudaStream_t stream, bool bulk = false);
+                  cudaStream_t stream, bool bulk = false, bool one_body = false);
 
 }  // namespace sdmrg

@@ -383,3 +383,25 @@ def test_in_place_arena_fill_matches_dense_arenas():
     a, b = p_in.apply(x), p_dense.apply(x)
     assert torch.equal(a, b)
     assert a.abs().max().item() > 0
+
+
+@pytest.mark.parametrize("stack", ["1", "0"])
+def test_engine_variants_bitwise_equal(monkeypatch, stack):
+    """The phase-2 single-body engine instance (always scaling: x * 1.0 == x)
+    and the stacked phase-1 products (same T values, wider ld) give bitwise
+    the same σ as the two-body / per-operator forms, and match the oracle."""
+    from paper_2305_05581_b200.plan import DevicePlan
+    from paper_2305_05581_b200.workload import fill_arenas_host, synthetic_plan_input
+    pi = fill_arenas_host(synthetic_plan_input(12, 96, seed=4), seed=4)
+    if stack == "0":
+        monkeypatch.setenv("SDMRG_NO_STACK_T", "1")
+    psi = np.random.default_rng(9).standard_normal(int(pi.psi_offsets()[-1]))
+    outs = []
+    for one in ("0", "1"):
+        monkeypatch.setenv("SDMRG_ONE_BODY", one)
+        plan = DevicePlan(pi)
+        outs.append(plan.apply(torch.from_numpy(psi).cuda()).cpu())
+        plan.close()
+    assert torch.equal(outs[0], outs[1])
+    ref = heff.apply_groups(pi, heff.build_groups(pi), psi)
+    assert rel_err(outs[0].numpy(), ref) <= 1e-12
