@@ -249,20 +249,24 @@ int upload_vec(const std::vector<T>& v, T** out) {
 
 // Split-K granule = 1/split_factor of one persistent CTA's share of the
 // phase-2 work (SDMRG_SPLIT overrides; experiments).
-// Phase-2 engine instance: the single-body one when less than half of the
-// work sits in full 8 x 8-block tiles (every warp on the 4 x 4 body): a wide
-// tile-shape mix is what overflows the instruction cache.  L=30 D=2048 (56%
-// full) keeps two bodies (1.3 ms faster); L=50 D=4096 (40%) takes one
-// (6 ms faster, profiles/r1_notes.md).  SDMRG_ONE_BODY=0/1 forces it.
+// Phase-2 engine instance: the single-body one when the work is spread over
+// many tile shapes (8-row x 8-column block counts) — a wide shape mix is what
+// overflows the instruction cache.  Criterion: the three most common shapes
+// carry < 40% of the phase-2 work (L=30 D=2048: 53% -> two bodies, 0.3-1.2 ms
+// faster; L=50 D=4096: 31% -> one body, 6 ms faster; profiles/r1_notes.md).
+// SDMRG_ONE_BODY=0/1 forces it.
 bool use_one_body(const GemmBatch& gb) {
   const char* env = getenv("SDMRG_ONE_BODY");
   if (env) return atoi(env) != 0;
-  double full = 0.0, all = 0.0;
+  std::vector<double> by_shape(9 * 9, 0.0);
+  double all = 0.0;
   for (size_t t = 0; t < gb.tiles.size(); ++t) {
+    const int mb = std::min((gb.tiles[t].tm + 7) / 8, 8), nb = std::min((gb.tiles[t].tn + 7) / 8, 8);
+    by_shape[mb * 9 + nb] += gb.tile_cost[t];
     all += gb.tile_cost[t];
-    if (gb.tiles[t].tm > 56 && gb.tiles[t].tn > 56) full += gb.tile_cost[t];
   }
-  return all > 0.0 && full < 0.5 * all;
+  std::sort(by_shape.begin(), by_shape.end(), std::greater<double>());
+  return all > 0.0 && by_shape[0] + by_shape[1] + by_shape[2] < 0.4 * all;
 }
 int p2_octaves() {
   static const int v = getenv("SDMRG_P2_OCTAVES") ? atoi(getenv("SDMRG_P2_OCTAVES")) : 0;
