@@ -861,8 +861,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       ch.comb3.add_tasks(out_first, static_cast<int>(qr));
       ch.bytes3 += 8LL * (co.term_end - co.term_begin + 1) * qr;
     }
-    ch.host1.finalize_tiles();
-    ch.host2.finalize_tiles(p2_octaves());
+    ch.host1.finalize_tiles(0, getenv("SDMRG_P1_BY_PROBLEM") != nullptr);
+    ch.host2.finalize_tiles(p2_octaves(), getenv("SDMRG_P2_BY_PROBLEM") != nullptr);
     ch.p2_one_body = use_one_body(ch.host2);
     ch.ws_doubles = ws;
     tiles += (int64_t)(ch.host1.tiles.size() + ch.host2.tiles.size());

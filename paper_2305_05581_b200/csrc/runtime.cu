@@ -134,11 +134,19 @@ void GemmBatch::append(GemmBatch&& o) {
   o = GemmBatch();
 }
 
-void GemmBatch::finalize_tiles(int octaves) {
+void GemmBatch::finalize_tiles(int octaves, bool by_problem) {
   // stable descending-cost order by bucketing on the (few) distinct costs:
   // O(n + u log u) instead of a comparison sort of millions of tiles
   if (octaves > 0)
     for (double& c : tile_cost) c = std::exp2(std::floor(std::log2(c) * octaves) / octaves);
+  std::vector<double> own;
+  if (by_problem) {  // sort keys: the problem's largest tile cost
+    own = tile_cost;
+    std::vector<double> pmax(probs.size(), 0.0);
+    for (size_t i = 0; i < tiles.size(); ++i)
+      pmax[tiles[i].prob] = std::max(pmax[tiles[i].prob], tile_cost[i]);
+    for (size_t i = 0; i < tiles.size(); ++i) tile_cost[i] = pmax[tiles[i].prob];
+  }
   std::vector<double> uniq(tile_cost);
   std::sort(uniq.begin(), uniq.end(), std::greater<double>());
   uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
@@ -155,7 +163,7 @@ void GemmBatch::finalize_tiles(int octaves) {
   for (size_t i = 0; i < tiles.size(); ++i) {
     const int64_t dst = start[bucket[i]]++;
     t2[dst] = tiles[i];
-    c2[dst] = tile_cost[i];
+    c2[dst] = by_problem ? own[i] : tile_cost[i];  // the tile's own cost
   }
   tiles.swap(t2);
   tile_cost.swap(c2);

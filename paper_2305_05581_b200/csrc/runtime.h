@@ -43,7 +43,9 @@ struct GemmBatch {
   // order tiles by descending cost (longest-processing-time first)
   // octaves > 0: costs bucketed to 1/octaves of a power of two (emission
   // order kept inside a bucket) instead of exact distinct costs
-  void finalize_tiles(int octaves = 0);
+  // by_problem: order by each problem's largest tile cost, a problem's tiles
+  // kept together (sibling tiles share operand panels in L2)
+  void finalize_tiles(int octaves = 0, bool by_problem = false);
   int upload(DeviceBatch* out, cudaStream_t stream) const;
   int64_t flops() const;  // useful (unpadded) FLOPs
 };
