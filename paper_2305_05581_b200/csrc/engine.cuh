@@ -184,14 +184,36 @@ __host__ __device__ constexpr int stage_elems() { return a_elems<TA>() + b_elems
 // Per-stage metadata written by the producer's lane 0.
 struct StageMeta {
   double* c;         // tile origin in C (first stage of a tile)
-  double scale;
+  double scale;      // != 1: some k4 step of the stage is scaled
+  double kscale[4];  // scale of each k4 step (packed stages: one per segment piece)
   int32_t nks;       // k4 steps in this stage (0: no K, or kEnd)
   int32_t flags;
   int32_t ldc, beta;
   int16_t tm, tn;
   int32_t pad;
 };
-constexpr int kFirst = 1, kLast = 2, kEnd = 4;
+constexpr int kFirst = 1, kLast = 2, kEnd = 4, kPacked = 8;
+// Segment packing (aligned path): a stage's 16 k rows are filled from as many
+// consecutive segments of the tile as fit, each starting on a k4 boundary
+// with its own scale per k4 step — short segments (small sectors: K = a few
+// states) no longer cost one ring stage each (L=30 D=512: 1.5x fewer phase-2
+// stages, D=2048: 1.09x).
+#ifndef SDMRG_PACK
+#define SDMRG_PACK 0
+#endif
+#ifndef SDMRG_PACK_P2
+#define SDMRG_PACK_P2 0
+#endif
+// Measured (profiles/r1_notes.md): packing made phase 2 13-17% slower (and
+// 1.8x slower at D=512) even with uniform-scale stages only (SDMRG_PACK=2),
+// and phase 1 (one segment per tile) neutral — off by default; build
+// variants SDMRG_PACK=1/2 (+ SDMRG_PACK_P2=1 for the phase-2 instance) are
+// parity-tested.
+template <bool TB>
+__host__ __device__ constexpr bool pack_path() {
+  return SDMRG_PACK && (TB || SDMRG_PACK_P2);
+}
+static_assert(!(SDMRG_PACK && (SDMRG_LDS128 || SDMRG_DB)), "packing needs the natural k order");
 
 template <bool TA, bool TB>
 __host__ __device__ constexpr int smem_bytes() {
@@ -300,6 +322,10 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
     const int flags = m.flags;
     const int nks = m.nks;
     const double scale = m.scale;
+    // per-k4-step scale (packed stages; an LDS issued with the step's
+    // fragment loads); the whole-stage scale otherwise
+    const uint32_t ksc_addr = static_cast<uint32_t>(__cvta_generic_to_shared(&m.kscale[0]));
+    auto ksc = [&](int ks) { return pack_path<TB>() && SDMRG_PACK == 1 ? lds64(ksc_addr + 8 * ks) : scale; };
     const uint32_t a0 = ring.smem + stage * STAGE_B + a_off;
     const uint32_t b0 = ring.smem + stage * STAGE_B + b_off;
 #if SDMRG_DB
@@ -409,12 +435,13 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
 #pragma unroll
             for (int j = 0; j < NB; ++j) bf[j] = lds64(b0 + ks * B_KS + j * B_J);
             if (SCALED) {
+              const double sk = ksc(ks);
               if (NB <= MB) {
 #pragma unroll
-                for (int j = 0; j < NB; ++j) bf[j] *= scale;
+                for (int j = 0; j < NB; ++j) bf[j] *= sk;
               } else {
 #pragma unroll
-                for (int i = 0; i < MB; ++i) af[i] *= scale;
+                for (int i = 0; i < MB; ++i) af[i] *= sk;
               }
             }
 #ifndef SDMRG_EXP_NOMMA
@@ -628,6 +655,43 @@ __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const doubl
   }
 }
 
+// Packed-stage variant: stage k rows [kb, kb + len) (kb, len multiples of 4)
+// from source k rows [0, len), rows >= valid zero-filled; the stage's other
+// rows belong to other segments and are not touched.
+template <bool KCONTIG, int NC_LD, int CAP>
+__device__ __forceinline__ void load_operand_range(uint32_t sbase, const double* src, int ld,
+                                                   int extent, int kb, int len, int valid,
+                                                   int lane) {
+  if (KCONTIG) {
+    const int k = 2 * (lane & 7), r0 = lane >> 3;
+    if (k < kb || k >= kb + len) return;
+    const int kk = k - kb;
+    const int bytes = kk + 1 < valid ? 16 : (kk < valid ? 8 : 0);
+    const double* p = bytes ? src + (int64_t)r0 * ld + kk : src;
+    const int64_t step = bytes ? 4 * (int64_t)ld : 0;
+    const uint32_t s0 = sbase + (r0 * KC_LD + k) * 8;
+    const int nrow = (extent - r0 + 3) >> 2;
+#pragma unroll 4
+    for (int i = 0; i < nrow; ++i) cp_async16(s0 + i * (4 * KC_LD * 8), p + i * step, bytes);
+  } else {
+#pragma unroll
+    for (int j = 0; j < (CAP + 63) / 64; ++j) {
+      const int c = 2 * lane + 64 * j;
+      if (c < extent) {
+        const double* p = src + c;
+        const uint32_t s0 = sbase + c * 8;
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+          const int kk = k - kb;
+          if (kk >= 0 && kk < len)
+            cp_async16(s0 + k * (NC_LD * 8), kk < valid ? p + (int64_t)kk * ld : src,
+                       kk < valid ? 16 : 0);
+        }
+      }
+    }
+  }
+}
+
 // L2 prefetch of one contiguous element range with a single bulk (TMA-unit)
 // prefetch: the range is widened to 16-byte alignment.
 __device__ __forceinline__ void bulk_prefetch_l2(const double* first, const double* last) {
@@ -677,6 +741,8 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
       m.nks = nks;
       m.scale = scale;
       m.flags = flags;
+      if (!(flags & kPacked))
+        m.kscale[0] = m.kscale[1] = m.kscale[2] = m.kscale[3] = scale;
       if (flags & kFirst) {
         m.c = cptr;
         m.ldc = tr.ldc;
@@ -739,6 +805,9 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
       if (next < ntiles && nrec.seg_begin < nrec.seg_end) sn = segs[nrec.seg_begin];
     }
     bool first = true;
+    int kfill = 0;           // packed rows in the open stage (multiple of 4)
+    double open_scale = 1.0; // SDMRG_PACK == 2: the open stage's (uniform) scale
+    bool unit = true;        // every k4 step of the open stage unscaled
     for (int s = cur.seg_begin; s < cur.seg_end; ++s) {
       const Seg sg = sn;
       if (s + 1 < cur.seg_end) {
@@ -759,6 +828,84 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
       const bool btiled = !TB && BULK && sg.btile > 0;
       if (btiled) b += (int64_t)(cur.col0 / cur.colw) * sg.btile * NC_LD_B;
       else b += TB ? (int64_t)cur.col0 * sg.ldb : cur.col0;
+      if (pack_path<TB>() && BULK && !btiled) {
+        if (SDMRG_PACK == 2 && kfill > 0 &&
+            __double_as_longlong(sg.scale) != __double_as_longlong(open_scale)) {
+          // uniform-scale stages: close the open one before a new scale
+          meta_write(stage, kfill >> 2, open_scale, (first ? kFirst : 0), cur, cptr);
+          __syncwarp();
+          mbar_arrive_cp_async(ring.full0 + 8 * stage);
+          if (lane == 0 && leader) mbar_arrive(ring.full0 + 8 * stage);
+          first = false;
+          kfill = 0;
+          unit = true;
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        open_scale = sg.scale;
+        for (int k0 = 0; k0 < sg.k;) {
+          if (kfill == 0) mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
+          const uint32_t sa = ring.smem + stage * STAGE_B;
+          const uint32_t sb = sa + A_EL * 8;
+          const int valid = min(BK - kfill, sg.k - k0);
+          const int len = min(BK - kfill, (sg.k - k0 + 3) & ~3);
+          const double* asrc = TA ? a + (int64_t)k0 * sg.lda : a + k0;
+          const double* bsrc = TB ? b + k0 : b + (int64_t)k0 * sg.ldb;
+#ifndef SDMRG_EXP_NOLOAD
+          if (kfill == 0 && len == BK) {
+            if (load_a) load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, valid, lane);
+            if (load_b) load_operand_aligned<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, valid, lane);
+          } else {
+            if (load_a)
+              load_operand_range<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, kfill, len, valid, lane);
+            if (load_b)
+              load_operand_range<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, kfill, len, valid, lane);
+          }
+#endif
+          if (lane == 0 && leader) {
+            StageMeta& m = ring.meta[stage];
+            for (int q = kfill >> 2; q < (kfill + len) >> 2; ++q) m.kscale[q] = sg.scale;
+          }
+          unit = unit && __double_as_longlong(sg.scale) == 0x3FF0000000000000LL;
+          kfill += len;
+          k0 += len;
+          const bool last = (s + 1 == cur.seg_end) && k0 >= sg.k;
+          if (kfill == BK || last) {
+            meta_write(stage, kfill >> 2, SDMRG_PACK == 2 ? open_scale : (unit ? 1.0 : 2.0),
+                       (SDMRG_PACK == 2 ? 0 : kPacked) | (first ? kFirst : 0) | (last ? kLast : 0),
+                       cur, cptr);
+            __syncwarp();
+            const uint32_t full = ring.full0 + 8 * stage;
+            mbar_arrive_cp_async(full);
+            if (lane == 0 && leader) mbar_arrive(full);
+            first = false;
+            kfill = 0;
+            unit = true;
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+        continue;
+      }
+      if (kfill > 0) {
+        // a stage-tiled segment after packed ones: close the open stage
+        meta_write(stage, kfill >> 2, SDMRG_PACK == 2 ? open_scale : (unit ? 1.0 : 2.0),
+                   (SDMRG_PACK == 2 ? 0 : kPacked) | (first ? kFirst : 0), cur, cptr);
+        __syncwarp();
+        mbar_arrive_cp_async(ring.full0 + 8 * stage);
+        if (lane == 0 && leader) mbar_arrive(ring.full0 + 8 * stage);
+        first = false;
+        kfill = 0;
+        unit = true;
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
       for (int k0 = 0; k0 < sg.k; k0 += BK) {
         const int krem = min(BK, sg.k - k0);
         mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
