@@ -40,6 +40,11 @@ constexpr int COMB_THREADS = 256;
 constexpr int COMB_PER_THREAD = 4;
 constexpr int COMB_CHUNK = COMB_THREADS * COMB_PER_THREAD;
 
+// U > 1: the loads of U terms are issued before their FMAs (same summation
+// order, bitwise the same result) — for the split-K partial sums (phase 3),
+// whose long per-element term chains are latency-bound at small D.  Phase 0
+// (HBM-bound, many outputs) measured slower that way and keeps U = 1.
+template <int U>
 __global__ void __launch_bounds__(COMB_THREADS)
 combine_kernel(const CombTask* __restrict__ tasks, const CombOut* __restrict__ outs,
                const CombTerm* __restrict__ terms, Bases bases) {
@@ -49,7 +54,28 @@ combine_kernel(const CombTask* __restrict__ tasks, const CombOut* __restrict__ o
     double acc[COMB_PER_THREAD];
 #pragma unroll
     for (int u = 0; u < COMB_PER_THREAD; ++u) acc[u] = 0.0;
-    for (int k = out.term_begin; k < out.term_end; ++k) {
+    int k = out.term_begin;
+    if (U > 1) {
+      for (; k + U <= out.term_end; k += U) {
+        double v[U][COMB_PER_THREAD], cf[U];
+#pragma unroll
+        for (int x = 0; x < U; ++x) {
+          const CombTerm term = terms[k + x];
+          const double* src = resolve(bases, term.src) + t.e0;
+          cf[x] = term.coef;
+#pragma unroll
+          for (int u = 0; u < COMB_PER_THREAD; ++u) {
+            const int e = threadIdx.x + u * COMB_THREADS;
+            v[x][u] = e < t.ne ? __ldg(src + e) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < U; ++x)
+#pragma unroll
+          for (int u = 0; u < COMB_PER_THREAD; ++u) acc[u] = fma(cf[x], v[x][u], acc[u]);
+      }
+    }
+    for (; k < out.term_end; ++k) {
       const CombTerm term = terms[k];
       const double* src = resolve(bases, term.src) + t.e0;
 #pragma unroll

@@ -272,15 +272,28 @@ int p2_octaves() {
   static const int v = getenv("SDMRG_P2_OCTAVES") ? atoi(getenv("SDMRG_P2_OCTAVES")) : 0;
   return v;
 }
+// Floor of the split-K granule (tile cost units: rows x cols x K): parts
+// smaller than this cost more in tile start-up, partial-buffer writes and the
+// phase-3 sum (a serial chain over the parts per σ element) than their
+// balance gains — small-D plans only (D=2048's granule is ~10 M).
+double split_min() {
+  const char* e = getenv("SDMRG_SPLIT_MIN");
+  return e ? std::max(0.0, atof(e)) : 0.0;
+}
 double split_factor() {
   const char* e = getenv("SDMRG_SPLIT");
   return e ? std::max(1.0, atof(e)) : 96.0;
 }
 
-int launch_combine(const CombList& cl, const Bases& bases, cudaStream_t stream) {
+int launch_combine(const CombList& cl, const Bases& bases, cudaStream_t stream,
+                   bool latency_bound = false) {
   if (cl.ntasks == 0) return SDMRG_OK;
-  combine_kernel<<<static_cast<unsigned>(cl.ntasks), COMB_THREADS, 0, stream>>>(
-      cl.d_tasks, cl.d_outs, cl.d_terms, bases);
+  if (latency_bound && !getenv("SDMRG_COMB3_U1"))
+    combine_kernel<4><<<static_cast<unsigned>(cl.ntasks), COMB_THREADS, 0, stream>>>(
+        cl.d_tasks, cl.d_outs, cl.d_terms, bases);
+  else
+    combine_kernel<1><<<static_cast<unsigned>(cl.ntasks), COMB_THREADS, 0, stream>>>(
+        cl.d_tasks, cl.d_outs, cl.d_terms, bases);
   count_launch();
   return cuda_check(cudaGetLastError(), "combine_kernel launch");
 }
@@ -821,8 +834,9 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     auto tiles_of = [](int extent) { return (extent + BM - 1) / BM; };
     double total_cost = 0.0;
     for (const OutProb& op : outs) total_cost += double(op.q) * op.r * op.ksum;
-    const double granule =
-        total_cost / (double(d->dry_run ? 1 : engine_grid(false, false)) * split_factor()) + 1.0;
+    const double granule = std::max(
+        total_cost / (double(d->dry_run ? 1 : engine_grid(false, false)) * split_factor()) + 1.0,
+        split_min());
     for (const OutProb& op : outs) {
       const double tile_cost =
           double(op.q) / tiles_of(op.q) * (double(op.r) / tiles_of(op.r)) * op.ksum;
@@ -1119,7 +1133,7 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
       cudaEventRecord(ch.ev[5], stream);
       cudaEventRecord(ch.ev[6], stream);
     }
-    rc = launch_combine(ch.comb3, bases, stream);
+    rc = launch_combine(ch.comb3, bases, stream, true);
     if (rc) return rc;
     if (plan->timing) cudaEventRecord(ch.ev[7], stream);
   }
