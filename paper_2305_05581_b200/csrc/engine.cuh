@@ -201,6 +201,9 @@ constexpr int kFirst = 1, kLast = 2, kEnd = 4, kPacked = 8;
 #ifndef SDMRG_PACK
 #define SDMRG_PACK 0
 #endif
+#ifndef SDMRG_ROUND
+#define SDMRG_ROUND 0
+#endif
 #ifndef SDMRG_PACK_P2
 #define SDMRG_PACK_P2 0
 #endif
@@ -527,6 +530,18 @@ __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring&
                                                  uint32_t& phase, uint32_t a_off, uint32_t b_off,
                                                  double* c, int ldc, int beta, int row_lim,
                                                  int col_lim, int lane) {
+  if constexpr (ONE && SDMRG_ROUND) {
+    switch (mblk * 8 + nblk) {
+      SDMRG_TILE_CASE(4, 4) SDMRG_TILE_CASE(4, 2) SDMRG_TILE_CASE(4, 1)
+      SDMRG_TILE_CASE(2, 4) SDMRG_TILE_CASE(2, 2) SDMRG_TILE_CASE(2, 1)
+      SDMRG_TILE_CASE(1, 4) SDMRG_TILE_CASE(1, 2) SDMRG_TILE_CASE(1, 1)
+      default:
+        consume_tile<TA, TB, 0, 0, ONE>(ring, stage, phase, a_off, b_off, c, ldc, beta, row_lim,
+                                        col_lim, lane);
+        break;
+    }
+    return;
+  }
   if constexpr (grid_adapt<TB>()) {
     if (mblk > 4 || nblk > 4) {  // 1 x 4 / 4 x 1 warp grids of odd-block tiles
       switch (mblk * 8 + nblk) {
@@ -1045,8 +1060,16 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
     const uint32_t b_off =
         A_EL * 8 + (TB ? ((wc0 + lr) * KC_LD + kf) * 8 : (kf * NC_LD_B + wc0 + lr) * 8);
     double* c = m.c + (int64_t)(wr0 + lr) * m.ldc + wc0 + 2 * lc;
-    consume_dispatch<TA, TB, ONE>(mblk, nblk, ring, stage, phase, a_off, b_off, c, m.ldc, m.beta,
-                             tm - wr0 - lr, tn - wc0 - 2 * lc, lane);
+    if constexpr (ONE && SDMRG_ROUND) {
+      // 3 -> 4 blocks (the extra block's DMMAs are discarded: its stores are
+      // cut at the warp's own extent): 9 shape bodies instead of 16
+      const int re = min(tm - wr0, 8 * mblk) - lr, ce = min(tn - wc0, 8 * nblk) - 2 * lc;
+      consume_dispatch<TA, TB, ONE>(mblk == 3 ? 4 : mblk, nblk == 3 ? 4 : nblk, ring, stage, phase,
+                                    a_off, b_off, c, m.ldc, m.beta, re, ce, lane);
+    } else {
+      consume_dispatch<TA, TB, ONE>(mblk, nblk, ring, stage, phase, a_off, b_off, c, m.ldc,
+                                    m.beta, tm - wr0 - lr, tn - wc0 - 2 * lc, lane);
+    }
   }
 }
 
