@@ -5,8 +5,10 @@
 TAG=$1; shift
 OUT=gpurun_out/$TAG; mkdir -p $OUT
 IFS=';' read -ra CF <<< "${CFGS:-30 2048;50 4096}"
+ORDER=("$@"); REV=(); for ((x=${#ORDER[@]}-1; x>=0; x--)); do REV+=("${ORDER[x]}"); done
 for r in 1 2; do
-  for knob in "$@"; do
+  if [ $r = 1 ]; then LIST=("${ORDER[@]}"); else LIST=("${REV[@]}"); fi  # ABBA: cancels position bias
+  for knob in "${LIST[@]}"; do
     for cfg in "${CF[@]}"; do
       if [ "$knob" = none ]; then res=$(timeout 600 python tools/quick.py $cfg 2>&1 | tail -1)
       else res=$(env $knob timeout 600 python tools/quick.py $cfg 2>&1 | tail -1); fi
