@@ -28,6 +28,12 @@
  * sdmrg_rotate                    dmrg.py:254  _transform_tree (W^T O W for
  *                                 every maintained operator block)
  * sdmrg_rdm_accumulate            dmrg.py:221  rdm_eigensystem (ρ += S S^T)
+ * sdmrg_grouped_gemm              the block algebra of a sweep step on the same
+ *                                 engine: blocks.py:331 materialize_aux,
+ *                                 blocks.py:190 enlarge_block (+ :262 the
+ *                                 enlarged H) fused with dmrg.py:254
+ *                                 _transform_tree, driver.py:200/228 White's
+ *                                 prediction (paper_2305_05581_b200/blockops.py)
  *
  * Errors: every function returns SDMRG_OK (0) or a nonzero code and records a
  * message retrievable with sdmrg_last_error() (thread-local).  Argument errors
@@ -254,6 +260,23 @@ int sdmrg_rdm_accumulate(int64_t ntasks, const int64_t* s_off,
                          const int64_t* rho_off, const int32_t* rows,
                          const int32_t* cols, const double* base_s,
                          double* base_rho, void* stream);
+
+/* ------------------------------------------------- generic grouped GEMM --
+ * Row-major, stream-ordered (no host synchronisation).  For problem p:
+ *   C_p (m[p] x n[p], ldc[p]) = beta[p] * C_p
+ *        + sum_{s = seg_begin[p]}^{seg_begin[p+1]-1} scale[s] * op(A_s) op(B_s)
+ * op(A_s) is m x k[s]: A stored m x k (lda) or, trans_a, stored k x m (lda);
+ * op(B_s) is k[s] x n: B stored k x n (ldb) or, trans_b, stored n x k (ldb).
+ * Operands are handles: (base index << 60) | element offset, the base index
+ * selecting one of `nbases` (<= 8) device pointers in the HOST array `bases`.
+ * beta is 0 (overwrite; a problem without segments writes zeros) or 1.
+ * Segments of one problem are summed in order (deterministic).              */
+int sdmrg_grouped_gemm(int trans_a, int trans_b, int64_t nprob, const int64_t* c_h,
+                       const int32_t* ldc, const int32_t* m, const int32_t* n,
+                       const int32_t* beta, const int64_t* seg_begin, const int64_t* a_h,
+                       const int32_t* lda, const int64_t* b_h, const int32_t* ldb,
+                       const int32_t* k, const double* scale, double* const* bases,
+                       int nbases, void* stream);
 
 #ifdef __cplusplus
 }

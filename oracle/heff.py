@@ -151,3 +151,65 @@ def ref_flops(pi, groups):
         p = len(members)
         total += 2 * m * r * n * p + 2 * q * r * m * p
     return total
+
+
+def build_groups_fast(pi, key_subset=None):
+    """``build_groups`` vectorised over table rows (same grouping, same member
+    order, same folded scales, blocks.py:521-567): one numpy pass per ψ key.
+    ``key_subset``: iterable of ψ key indices to generate groups for (None =
+    all).  Used by the bench's CPU arm and the bench-scale parity tests, which
+    must not touch the product library."""
+    keys, _ = psi_layout(pi)
+    nk = len(keys)
+    nl, nr = len(pi.dim_l), len(pi.dim_r)
+    ns = pi.nsite
+    qn_l = [tuple(q) for q in pi.qn_l.tolist()]
+    qn_r = [tuple(q) for q in pi.qn_r.tolist()]
+    lidx = {q: j for j, q in enumerate(qn_l)}
+    ridx = {q: j for j, q in enumerate(qn_r)}
+
+    def shift_table(deltas, qns, idx):
+        tab = np.full((len(deltas), len(qns)), -1, np.int64)
+        for o, d in enumerate(deltas.tolist()):
+            for j, q in enumerate(qns):
+                tab[o, j] = idx.get(tuple(a + b for a, b in zip(q, d)), -1)
+        return tab
+
+    lsh = shift_table(pi.delta_l, qn_l, lidx)
+    rsh = shift_table(pi.delta_r, qn_r, ridx)
+    key3 = np.full((nl, ns, ns), -1, np.int64)
+    keyr = np.array([k[3] for k in keys], np.int64)
+    for i, (jl, s1, s2, _jr) in enumerate(keys):
+        key3[jl, s1, s2] = i
+    lop = pi.lop.astype(np.int64)
+    rop = pi.rop.astype(np.int64)
+    alpha = pi.alpha
+    e_l = pi.e_l != 0
+    out = []
+    subset = range(nk) if key_subset is None else sorted(int(i) for i in key_subset)
+    for i in subset:
+        jl, s1, s2, jr = keys[i]
+        d1 = pi.site1_dst[:, s1].astype(np.int64)
+        d2 = pi.site2_dst[:, s2].astype(np.int64)
+        jlp = lsh[lop, jl]
+        jrp = rsh[rop, jr]
+        ok = (d1 >= 0) & (d2 >= 0) & (jlp >= 0) & (pi.blk_off_l[lop, jl] >= 0) \
+            & (jrp >= 0) & (pi.blk_off_r[rop, jr] >= 0)
+        o = np.full(len(lop), -1, np.int64)
+        o[ok] = key3[jlp[ok], d1[ok], d2[ok]]
+        ok &= o >= 0
+        ok[ok] &= keyr[o[ok]] == jrp[ok]
+        scale = alpha * pi.site1_val[:, s1] * pi.site2_val[:, s2]
+        scale = np.where(e_l, scale * pi.left_sign[jl], scale)
+        ok &= scale != 0.0
+        rows = np.nonzero(ok)[0]
+        if rows.size == 0:
+            continue
+        oo = o[rows]
+        order = np.argsort(oo, kind="stable")
+        rows, oo = rows[order], oo[order]
+        cuts = np.nonzero(np.diff(oo))[0] + 1
+        for seg_rows, seg_o in zip(np.split(rows, cuts), np.split(oo, cuts)):
+            out.append((i, int(seg_o[0]),
+                        list(zip(seg_rows.tolist(), scale[seg_rows].tolist()))))
+    return out

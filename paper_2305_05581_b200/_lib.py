@@ -97,6 +97,9 @@ _SIGS = {
     "sdmrg_rotate": (c_int, [c_i64, P_i64, P_i64, P_i64, P_i64, P_i32, P_i32, P_i32, P_i32,
                              c_vp, c_vp, c_vp, c_vp, c_i64, c_vp]),
     "sdmrg_rdm_accumulate": (c_int, [c_i64, P_i64, P_i64, P_i32, P_i32, c_vp, c_vp, c_vp]),
+    "sdmrg_grouped_gemm": (c_int, [c_int, c_int, c_i64, P_i64, P_i32, P_i32, P_i32, P_i32, P_i64,
+                                   P_i64, P_i32, P_i64, P_i32, P_i32, P_dbl,
+                                   ctypes.POINTER(c_vp), c_int, c_vp]),
 }
 
 EXPORTED = tuple(_SIGS)

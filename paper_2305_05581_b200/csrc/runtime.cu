@@ -5,6 +5,8 @@
 #include <functional>
 #include <atomic>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <numeric>
 
 #include "../../include/sdmrg_b200.h"
@@ -27,24 +29,31 @@ int cuda_check(cudaError_t e, const char* what) {
 }
 void count_launch(int n) { g_launches += n; }
 
+// Persistent grid per (device, TA, TB): the dynamic shared-memory opt-in is a
+// per-device function attribute, so it is set once on every device the
+// process launches on (a process-wide static broke device 1+).
 template <bool TA, bool TB>
 static int grid_for() {
-  static int grid = 0;
-  if (grid == 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(seg_gemm_kernel<TA, TB, false>,
+  static std::mutex mu;
+  static std::map<int, int> grids;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = grids.find(dev);
+  if (it != grids.end()) return it->second;
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(seg_gemm_kernel<TA, TB, false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<TA, TB>());
+  cudaFuncSetAttribute(seg_gemm_kernel<TA, TB, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<TA, TB>());
+  if (!TA && !TB)
+    cudaFuncSetAttribute(seg_gemm_kernel<false, false, true, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<TA, TB>());
-    cudaFuncSetAttribute(seg_gemm_kernel<TA, TB, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<TA, TB>());
-    if (!TA && !TB)
-      cudaFuncSetAttribute(seg_gemm_kernel<false, false, true, true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<TA, TB>());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, seg_gemm_kernel<TA, TB, true>, THREADS,
-                                                  smem_bytes<TA, TB>());
-    grid = sms * std::max(per, 1);
-  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, seg_gemm_kernel<TA, TB, true>, THREADS,
+                                                smem_bytes<TA, TB>());
+  const int grid = sms * std::max(per, 1);
+  grids[dev] = grid;
   return grid;
 }
 

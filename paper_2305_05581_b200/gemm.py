@@ -107,8 +107,14 @@ class CudaGemm:
         _check_dims(a, b, c)
         m, k = a.shape
         n = b.shape[1]
-        if isinstance(c, torch.Tensor) and c.is_cuda and (c.stride(0) == 1 or n == 1):
+        if isinstance(c, torch.Tensor) and c.is_cuda and c.stride(0) == 1:
             self._gemm_dev(_dev(a, self.device), _dev(b, self.device), c, alpha, beta)
+        elif isinstance(c, torch.Tensor) and c.is_cuda:
+            # strided device output (e.g. a column slice of a row-major
+            # tensor): compute into a column-major temporary
+            cd = c.t().contiguous().t()
+            self._gemm_dev(_dev(a, self.device), _dev(b, self.device), cd, alpha, beta)
+            c.copy_(cd)
         else:
             ch = c if isinstance(c, np.ndarray) else c.cpu().numpy()
             cd = torch.from_numpy(np.asfortranarray(ch, dtype=np.float64)).to(self.device)

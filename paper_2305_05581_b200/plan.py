@@ -22,11 +22,27 @@ except ImportError:  # pragma: no cover - torch is part of the image
     torch = None
 
 
-def _stream_handle(stream=None):
+def _stream_handle(stream=None, device=None):
     if torch is None or not torch.cuda.is_available():
         return None
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream
+
+
+class _on_device:
+    """Make the plan's device current around a library call (the library
+    allocates and launches on the current device)."""
+
+    def __init__(self, device):
+        self.ctx = torch.cuda.device(device) if device is not None else None
+
+    def __enter__(self):
+        if self.ctx is not None:
+            self.ctx.__enter__()
+
+    def __exit__(self, *exc):
+        if self.ctx is not None:
+            self.ctx.__exit__(*exc)
 
 
 def _desc(pi, arena_l=None, arena_r=None, rank=0, world=1, workspace_doubles=0,
@@ -117,7 +133,8 @@ class DevicePlan:
         self._desc = _desc(self.pi, self.arena_l, self.arena_r, rank, world,
                            workspace_doubles, keep_groups, dry_run)
         handle = ctypes.c_void_p()
-        _lib.check(lib.sdmrg_plan_build(ctypes.byref(self._desc), ctypes.byref(handle)))
+        with _on_device(self.device):
+            _lib.check(lib.sdmrg_plan_build(ctypes.byref(self._desc), ctypes.byref(handle)))
         self._h = handle
         # the library repacked the arenas into plan-owned padded memory: the
         # caller's (or our temporary device) copies are no longer referenced
@@ -134,6 +151,7 @@ class DevicePlan:
         self.keys = keys
         self.offsets = offs
         self.keep_groups = keep_groups
+        self.counter = None     # backend.counter of the drop-in apply_plan
 
     # reference-facing attributes (blocks.py:495 EffectiveHamiltonianPlan)
     @property
@@ -202,8 +220,14 @@ class DevicePlan:
                     and v.numel() == self.psi_size):
                 raise ValueError("apply: vectors must be contiguous float64 CUDA tensors "
                                  f"of length {self.psi_size}")
-        _lib.check(_lib.load().sdmrg_plan_apply(self._h, psi.data_ptr(), sigma.data_ptr(),
-                                                int(bool(accumulate)), _stream_handle(stream)))
+        if psi.device != self.device or sigma.device != self.device:
+            raise ValueError(f"apply: vectors must live on the plan's device {self.device}")
+        with _on_device(self.device):
+            _lib.check(_lib.load().sdmrg_plan_apply(
+                self._h, psi.data_ptr(), sigma.data_ptr(), int(bool(accumulate)),
+                _stream_handle(stream, self.device)))
+        if self.counter is not None:   # reference accounting (sbmm4s.py:190 via gemm.py:22)
+            self.counter.count(multiplies=2 * self.stats["groups"], flops=self.flops)
         return sigma
 
     __call__ = apply
@@ -229,7 +253,8 @@ class DevicePlan:
 
     def close(self):
         if getattr(self, "_h", None):
-            _lib.load().sdmrg_plan_destroy(self._h)
+            with _on_device(self.device):
+                _lib.load().sdmrg_plan_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -259,6 +284,8 @@ def apply_plan(plan, psi, out, pool=None, arenas=None, backend=None, locks=None)
     its scheduling (persistent CTAs) and needs no per-sector locks because
     every σ tile has exactly one owner.
     """
+    if backend is not None and getattr(backend, "counter", None) is not None:
+        plan.counter = backend.counter      # driver.py:138 reads counter.snapshot()[2]
     if torch is not None and isinstance(psi, torch.Tensor):
         return plan.apply(psi, out, accumulate=True)
     vec = psi.to_vector()

@@ -1,0 +1,22 @@
+#!/bin/bash
+# Round-2 GPU pass: GPU parity tests, the bench line (default L=50 D=4096),
+# the reference arm, the ncu launch list of the bench command and full ncu
+# captures of one phase-1 and one phase-2 launch of the bench workload.
+# Usage: tools/gpu_r2.sh TAG [skip-tests]
+TAG=${1:-r2}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $OUT/gpu.txt 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+if [ "$2" != "skip-tests" ]; then
+  timeout 1800 python -m pytest tests -q -m gpu -x > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+fi
+timeout 900 python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --scale "" > $OUT/bench_under_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_gemm_kernel -s 2 -c 1 \
+    -o $OUT/prof_p1 python tools/prof_apply.py 50 4096 2 > $OUT/ncu_p1.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_gemm_kernel -s 3 -c 1 \
+    -o $OUT/prof_p2 python tools/prof_apply.py 50 4096 2 > $OUT/ncu_p2.log 2>&1
+ls -la $OUT
