@@ -124,7 +124,10 @@ class DevicePlan:
         if not dry_run:
             if torch is None or not torch.cuda.is_available():
                 raise _lib.LibraryError("DevicePlan needs a CUDA device (no CPU fallback)")
-            self.device = torch.device(device if device is not None else "cuda")
+            dev = torch.device(device if device is not None else "cuda")
+            if dev.index is None:
+                dev = torch.device("cuda", torch.cuda.current_device())
+            self.device = dev
             if not empty_arenas:
                 self.arena_l = arena_l if arena_l is not None else \
                     torch.from_numpy(self.pi.arena_l).to(self.device)
