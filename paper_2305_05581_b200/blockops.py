@@ -281,12 +281,9 @@ def composites(store, defs, model, device):
 
     # one- and two-factor strings: out_class = K @ store_class
     direct = np.nonzero(nf <= 2)[0]
-    lk = {}
     for t in direct.tolist():
-        key = op_key(inside[t])
-        if not ops.has(key):
-            raise KeyError(f"operator {key} not maintained on block {store.sites}")
-        lk.setdefault(key, []).append(t)
+        if not ops.has(op_key(inside[t])):
+            raise KeyError(f"operator {op_key(inside[t])} not maintained on block {store.sites}")
     _class_gemm(out, keys, ops, aux, coef, direct, [op_key(inside[t]) for t in direct.tolist()])
     # three-factor strings: M_(c, head) = Σ c · P (GEMM), out += Σ_head C · M
     three = np.nonzero(nf == 3)[0]
@@ -497,7 +494,10 @@ def enlarge_rotate(old, comp, local, terms, new_keys, fused, w, new_basis, devic
             t_list.append((pc[4], pc[5], pc[6], pc[7], pc[8], pc[2]))   # base, xoff, dr, dc, wc, n
     t_off = np.zeros(len(t_list) + 1, np.int64)
     t_off[1:] = np.cumsum([t[2] * t[5] for t in t_list])
-    budget = t_budget or max(1 << 24, int(0.25 * torch.cuda.mem_get_info(device)[0] / 8))
+    if t_budget is None:
+        free = torch.cuda.mem_get_info(device)[0] if device.type == "cuda" else 1 << 33
+        t_budget = max(1 << 24, int(0.25 * free / 8))
+    budget = t_budget
     # chunk the pieces by output so each chunk's T fits the budget
     order = sorted(range(len(pieces)), key=lambda i: pieces[i][0])
     chunks, cur, cur_t, seen = [], [], 0, set()

@@ -1,0 +1,111 @@
+"""Closed-loop device DMRG against the reference's own recorded runs.
+
+The driver (paper_2305_05581_b200/driver.py) runs warm-up + sweeps with
+NOTHING from the reference at run time: its own factorization of the same
+integrals, device block stores grown/truncated/partially summed on the
+engine, the device H_eff·ψ plan and Lanczos, White's prediction.  The
+reference's records come from ``driver.py:356 solve`` itself
+(tests/golden/make_sweep_record.py, make_sweep_golden.py).
+
+North star: sweep energies within 1e-8 Eh.  Tested per iteration (every
+recorded two-site step, same position/direction order), plus the
+truncation errors and, where the runs are short enough to be
+rounding-insensitive, the Lanczos iteration counts.
+"""
+
+import glob
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = os.path.join(HERE, "golden")
+E_TOL = 1e-8
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _load_record(name):
+    rows = [json.loads(x) for x in open(os.path.join(GOLDEN, name))]
+    hdr = rows[0]
+    return hdr, [r for r in rows[1:] if "sweep" in r]
+
+
+def _run(n, model_seed, run_seed, d, sweeps, tol, max_iter, limit=None, scale=0.2, core=0.3):
+    from paper_2305_05581_b200 import driver as drv
+    from paper_2305_05581_b200 import model as M
+    mm = M.Model(M.random_integrals(n, model_seed, scale=scale, core=core))
+    sch = drv.SweepSchedule(n_sweeps=sweeps, d=d, lanczos_tol=tol, lanczos_max_iter=max_iter)
+    st = drv.warmup(mm, sch, seed=run_seed)
+    if limit is None or len(st.records) < limit:
+        drv.run_sweeps(st, sch)
+    return st.records
+
+
+def _compare(mine, ref, check_iters=True):
+    assert len(mine) >= len(ref)
+    worst = 0.0
+    for a, b in zip(mine, ref):
+        assert (a.sweep, a.position, a.direction) == (b["sweep"], b["position"], b["direction"])
+        de = abs(a.energy - b["energy"])
+        worst = max(worst, de)
+        assert de <= E_TOL, (a.sweep, a.position, a.direction, a.energy, b["energy"])
+        assert abs(a.truncation_error - b["truncation_error"]) <= 1e-8
+        if check_iters:
+            assert abs(a.lanczos_iterations - b["lanczos_iterations"]) <= 2
+    return worst
+
+
+def test_closed_loop_golden_L6_D16():
+    """tests/golden/make_sweep_golden.py run: L=6, D=16, 2 sweeps."""
+    files = sorted(glob.glob(os.path.join(GOLDEN, "sweep_ints6_d16", "iter_*.npz")))
+    ref = []
+    for f in files:
+        z = np.load(f)
+        ref.append({"sweep": int(z["sweep"]), "position": int(z["position"]),
+                    "direction": str(z["direction"]), "energy": float(z["energy"]),
+                    "truncation_error": None, "lanczos_iterations": int(z["iterations"])})
+    from paper_2305_05581_b200 import driver as drv
+    from paper_2305_05581_b200 import model as M
+    mm = M.Model(M.random_integrals(6, 21))
+    sch = drv.SweepSchedule(n_sweeps=2, d=16, lanczos_tol=1e-10)
+    res = drv.solve(mm, sch, seed=5)
+    assert len(res.records) == len(ref)
+    for a, b in zip(res.records, ref):
+        assert (a.sweep, a.position, a.direction) == (b["sweep"], b["position"], b["direction"])
+        assert abs(a.energy - b["energy"]) <= E_TOL
+
+
+@pytest.mark.parametrize("name", ["sweep_record_L5_D8.jsonl", "sweep_record_L8_D32.jsonl",
+                                  "sweep_record_L10_D64.jsonl"])
+def test_closed_loop_recorded_runs(name):
+    if not os.path.exists(os.path.join(GOLDEN, name)):
+        pytest.skip(f"{name} not recorded")
+    hdr, ref = _load_record(name)
+    mine = _run(hdr["L"], hdr["model_seed"], hdr["run_seed"], hdr["D"], hdr["sweeps"],
+                hdr["lanczos_tol"], hdr["lanczos_max_iter"])
+    _compare(mine, ref)
+
+
+def test_closed_loop_configs0_L16_D256():
+    """BASELINE configs[0]: L=16, D=256, 4 sweeps — every iteration the
+    reference finished recording (tests/golden/sweep_record_L16_D256.jsonl)."""
+    name = "sweep_record_L16_D256.jsonl"
+    if not os.path.exists(os.path.join(GOLDEN, name)):
+        pytest.skip("configs[0] record missing")
+    hdr, ref = _load_record(name)
+    if not ref:
+        pytest.skip("configs[0] record has no iterations yet")
+    mine = _run(hdr["L"], hdr["model_seed"], hdr["run_seed"], hdr["D"], hdr["sweeps"],
+                hdr["lanczos_tol"], hdr["lanczos_max_iter"])
+    _compare(mine, ref, check_iters=False)
