@@ -182,6 +182,9 @@ typedef struct sdmrg_plan_stats {
   int64_t build_ms_taskgen;        /* host: ψ keys, matching, pre-summation   */
   int64_t build_ms_emit;           /* host: work lists                        */
   int64_t build_ms_device;         /* repack, allocations, uploads            */
+  int64_t fused_outs;              /* σ problems on the fused small-sector    */
+                                   /* kernel (T chained in registers)         */
+  int64_t arena_bytes;             /* padded operator arenas held by the plan */
 } sdmrg_plan_stats;
 
 int sdmrg_plan_build(const sdmrg_plan_desc* desc, sdmrg_plan** out);

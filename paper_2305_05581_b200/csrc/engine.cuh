@@ -122,6 +122,9 @@ struct Seg {         // 40 B
 #endif
 // per-tile warp grid: 1 x 4 or 4 x 1 instead of 2 x 2 when a tile has an odd
 // number of 8-row (8-column) blocks, so the four DMMA warps stay balanced
+#ifndef SDMRG_ROTATE
+#define SDMRG_ROTATE 1
+#endif
 #ifndef SDMRG_GRID_ADAPT
 #define SDMRG_GRID_ADAPT 1
 #endif
@@ -1021,14 +1024,21 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
   }
 
   // ================================================================ consumers
-  const int wr = warp / WGRID_C, wc = warp % WGRID_C;
   const int lr = lane >> 2, lc = lane & 3;
   int stage = 0;
   uint32_t phase = 0;
+  // Warp roles rotate per tile (SDMRG_ROTATE): the balanced split of an odd
+  // block count gives role 0 the most blocks, and warp w of every CTA tends
+  // to sit on the same SM sub-partition (one FP64 pipe each) — rotating the
+  // roles spreads the heavy share over the four pipes.
+  int rot = SDMRG_ROTATE ? static_cast<int>(blockIdx.x) : 0;
   while (true) {
     mbar_wait(ring.full0 + 8 * stage, phase);
     const StageMeta& m = meta[stage];
     if (m.flags & kEnd) break;
+    const int vw = SDMRG_ROTATE ? (warp + rot) % CONSUMERS : warp;
+    rot += 1;
+    const int wr = vw / WGRID_C, wc = vw % WGRID_C;
     // first stage of a tile: balanced 2 x 2 warp split of its 8x8 blocks
     const int tm = m.tm, tn = m.tn;
     const int mb = (tm + 7) >> 3, nb = (tn + 7) >> 3;

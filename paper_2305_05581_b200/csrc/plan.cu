@@ -129,6 +129,7 @@ struct CombList {
 struct Chunk {
   GemmBatch host1, host2;  // released after upload
   DeviceBatch p1, p2;
+  FusedBatch fused;        // small-sector σ problems on the fused kernel (fused.cuh)
   CombList comb0;          // phase 0: pre-summed left operators
   CombList comb3;          // phase 3: split-K partial sums into σ
   int64_t ws_doubles = 0;
@@ -180,6 +181,7 @@ struct sdmrg_plan {
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
   sdmrg_plan_stats stats{};
+  int64_t fused_outs = 0;          // σ problems on the fused kernel
   int timing = 0;
 };
 
@@ -541,15 +543,38 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
 
   plan->mine = mine;
 
+  // ---- fused small-sector σ problems (fused.cuh): an out key whose rows q
+  // and every contributing ψ key's rows m are <= 64 is evaluated by the fused
+  // kernel (T = ψ R^T chained in registers, never stored); the others by the
+  // two-phase engine.  SDMRG_FUSED=0 turns the fused path off.
+  std::vector<char> fuse_out(nk, 0);
+  {
+    const char* fe = getenv("SDMRG_FUSED");
+    const bool allow = !(fe && fe[0] == '0');
+    if (allow) {
+      std::vector<int> maxm(nk, 0);
+      for (int64_t i = 0; i < nk; ++i) {
+        if (!mine[i]) continue;
+        for (const Pair& p : pairs[i])
+          maxm[p.out] = std::max(maxm[p.out], (int)d->dim_l[keys[i].jl]);
+      }
+      for (int64_t o = 0; o < nk; ++o)
+        fuse_out[o] = maxm[o] > 0 && maxm[o] <= 8 * F_MB && d->dim_l[keys[o].jl] <= 8 * F_QB;
+    }
+  }
+  plan->fused_outs = 0;
+  for (int64_t o = 0; o < nk; ++o) plan->fused_outs += fuse_out[o];
+
   // ---- execution schedule: chunks of ψ keys bounded by the workspace
-  // (distinct non-identity T blocks + pre-summed left operators per key)
+  // (distinct non-identity T blocks of two-phase products + pre-summed left
+  // operators per key)
   std::vector<int64_t> t_need(nk, 0), l_need(nk, 0);
   for (int64_t i = 0; i < nk; ++i) {
     if (!mine[i]) continue;
     const int64_t m = d->dim_l[keys[i].jl];
     std::vector<int32_t> rops;
     for (const Pair& p : pairs[i]) {
-      rops.push_back(p.rop);
+      if (!fuse_out[p.out]) rops.push_back(p.rop);
       if (p.term_end - p.term_begin > 1) l_need[i] += (int64_t)d->dim_l[keys[p.out].jl] * pad2(m);
     }
     std::sort(rops.begin(), rops.end());
@@ -646,7 +671,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       auto& tm = tmap[i - i0];
       std::vector<int32_t> rops;
       rops.reserve(pairs[i].size());
-      for (const Pair& pr : pairs[i]) rops.push_back(pr.rop);
+      for (const Pair& pr : pairs[i])
+        if (!fuse_out[pr.out]) rops.push_back(pr.rop);
       std::sort(rops.begin(), rops.end());
       rops.erase(std::unique(rops.begin(), rops.end()), rops.end());
       tm.reserve(rops.size());
@@ -765,33 +791,32 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       int q, r;
       int64_t ksum;
       std::vector<Seg> segs;
+      std::vector<FSeg> fsegs;  // fused σ problems: one product per entry
+      double fcost = 0.0;       // fused: DMMA work units of the whole problem
     };
     std::vector<OutProb> outs;
     outs.reserve(by_out.size());
     for (auto& kvp : by_out) {
       const int32_t o = kvp.first;
+      const bool fz = fuse_out[o] != 0;
       const auto& entries = *kvp.second;
       const int q = d->dim_l[keys[o].jl], r = d->dim_r[keys[o].jr];
-      OutProb op{o, q, r, 0, {}};
+      OutProb op{o, q, r, 0, {}, {}, 0.0};
       for (size_t u = 0; u < entries.size();) {
         const int64_t i = entries[u].first;
         const int m = d->dim_l[keys[i].jl];
+        const int n = d->dim_r[keys[i].jr];
         const int qm = q * pad2(m);  // a padded q x m block, pads included
         const int32_t out_first = static_cast<int32_t>(ch.comb0.outs.size());
         for (; u < entries.size() && entries[u].first == i; ++u) {
           const Pair& pr = *entries[u].second;
           const Term* tt = terms[i].data();
-          const TEntry& th = t_lookup(i, pr.rop);
-          Seg sg{};
-          sg.b = th.handle;
-          sg.ldb = th.ld;
-          sg.btile = th.btile;
-          sg.lda = pad2(m);
-          sg.k = m;
+          uint64_t ahandle;
+          double ascale;
           if (pr.term_end - pr.term_begin == 1) {
             const Term& t = tt[pr.term_begin];
-            sg.a = make_handle(B_ARENA_L, poff_l[(size_t)t.lop * nL + keys[i].jl]);
-            sg.scale = t.coef;
+            ahandle = make_handle(B_ARENA_L, poff_l[(size_t)t.lop * nL + keys[i].jl]);
+            ascale = t.coef;
           } else {
             const uint64_t lh = plan->lsum_persistent ? make_handle(B_LSUM, lsum_pos)
                                                       : make_handle(B_WS, ws);
@@ -802,8 +827,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
                    tt[x].coef});
             co.term_end = static_cast<int32_t>(ch.comb0.terms.size());
             ch.comb0.outs.push_back(co);
-            sg.a = lh;
-            sg.scale = 1.0;
+            ahandle = lh;
+            ascale = 1.0;
             if (plan->lsum_persistent) lsum_pos += qm;
             else ws += qm;
             ch.flops0 += 2LL * (co.term_end - co.term_begin) * qm;
@@ -811,10 +836,37 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
             ++comb_outputs;
             comb_terms += co.term_end - co.term_begin;
           }
-          op.segs.push_back(sg);
-          op.ksum += m;
-          exec_flops += 2LL * q * r * m;
-          ch.flops2 += 2LL * q * r * m;
+          if (fz) {
+            // fused product: T(i, b) = ψ_i R_b^T formed in registers per use
+            FSeg fs{};
+            fs.psi = make_handle(B_PSI, plan->poffs[i]);
+            fs.ident = d->kind_r[pr.rop] == 1;
+            fs.rb = fs.ident ? 0 : make_handle(B_ARENA_R, poff_r[(size_t)pr.rop * nR + keys[i].jr]);
+            fs.l = ahandle;
+            fs.m = m;
+            fs.n = n;
+            fs.scale = ascale;
+            op.fsegs.push_back(fs);
+            const int64_t f1 = fs.ident ? 0 : 2LL * m * n * r;
+            exec_flops += f1 + 2LL * q * r * m;
+            ch.flops2 += f1 + 2LL * q * r * m;
+            op.fcost += double((m + 7) / 8 * 8) * r * ((fs.ident ? 0 : (n + 3) / 4 * 4) + 2.0 * q);
+            op.ksum += m;
+          } else {
+            const TEntry& th = t_lookup(i, pr.rop);
+            Seg sg{};
+            sg.b = th.handle;
+            sg.ldb = th.ld;
+            sg.btile = th.btile;
+            sg.lda = pad2(m);
+            sg.k = m;
+            sg.a = ahandle;
+            sg.scale = ascale;
+            op.segs.push_back(sg);
+            op.ksum += m;
+            exec_flops += 2LL * q * r * m;
+            ch.flops2 += 2LL * q * r * m;
+          }
           ++products;
         }
         ch.comb0.add_tasks(out_first, qm);
@@ -830,25 +882,50 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     // σ block in step, so their shared operand panels hit in L2 — 1/6 was 5%
     // slower in phase 2) is cut into contiguous segment
     // ranges written to partial buffers; phase 3 adds them to σ in order
-    // (σ first, then parts 0..S-1: deterministic, no atomics).
+    // (σ first, then parts 0..S-1: deterministic, no atomics).  Fused σ
+    // problems use the same rule against the fused kernel's grid.
     auto tiles_of = [](int extent) { return (extent + BM - 1) / BM; };
-    double total_cost = 0.0;
-    for (const OutProb& op : outs) total_cost += double(op.q) * op.r * op.ksum;
+    double total_cost = 0.0, total_fcost = 0.0;
+    for (const OutProb& op : outs) {
+      if (!op.fsegs.empty()) total_fcost += op.fcost;
+      else total_cost += double(op.q) * op.r * op.ksum;
+    }
     const double granule = std::max(
         total_cost / (double(d->dry_run ? 1 : engine_grid(false, false)) * split_factor()) + 1.0,
         split_min());
+    const double fgranule =
+        total_fcost / (double(d->dry_run ? 148 : fused_grid_size()) * split_factor()) + 1.0;
     for (const OutProb& op : outs) {
-      const double tile_cost =
-          double(op.q) / tiles_of(op.q) * (double(op.r) / tiles_of(op.r)) * op.ksum;
-      int nsplit = static_cast<int>(std::min<double>(std::ceil(tile_cost / granule),
-                                                     double(op.segs.size())));
+      const bool fz = !op.fsegs.empty();
+      const size_t nseg = fz ? op.fsegs.size() : op.segs.size();
+      double tile_cost;
+      if (fz) {
+        const int rb = (op.r + 7) / 8, nt = (rb + F_RT - 1) / F_RT;
+        tile_cost = op.fcost / nt;
+      } else {
+        tile_cost = double(op.q) / tiles_of(op.q) * (double(op.r) / tiles_of(op.r)) * op.ksum;
+      }
+      int nsplit = static_cast<int>(std::min<double>(std::ceil(tile_cost / (fz ? fgranule : granule)),
+                                                     double(nseg)));
       nsplit = std::max(nsplit, 1);
       const uint64_t sig = make_handle(B_SIGMA, plan->offs[op.o]);
+      auto emit = [&](uint64_t c, int beta, size_t s0, size_t s1) {
+        if (fz) {
+          const int32_t fb = static_cast<int32_t>(ch.fused.segs.size());
+          ch.fused.segs.insert(ch.fused.segs.end(), op.fsegs.begin() + s0, op.fsegs.begin() + s1);
+          ch.fused.add_problem(c, op.r, op.q, op.r, beta, fb);
+        } else {
+          ch.host2.begin_prob(c, op.r, op.q, op.r, beta);
+          for (size_t x = s0; x < s1; ++x) {
+            const Seg& sg = op.segs[x];
+            ch.host2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale, sg.btile);
+          }
+          ch.host2.end_prob();
+        }
+      };
+      auto seg_k = [&](size_t x) { return fz ? op.fsegs[x].m : op.segs[x].k; };
       if (nsplit == 1) {
-        ch.host2.begin_prob(sig, op.r, op.q, op.r, 1);
-        for (const Seg& sg : op.segs)
-          ch.host2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale, sg.btile);
-        ch.host2.end_prob();
+        emit(sig, 1, 0, nseg);
         continue;
       }
       const int64_t qr = (int64_t)op.q * op.r;
@@ -857,16 +934,14 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       ch.comb3.terms.push_back({sig, 1.0});
       size_t u = 0;
       int64_t kdone = 0;
-      for (int sp = 0; sp < nsplit && u < op.segs.size(); ++sp) {
+      for (int sp = 0; sp < nsplit && u < nseg; ++sp) {
         const int64_t kcut = op.ksum * (sp + 1) / nsplit;
         const uint64_t part = make_handle(B_WS, ws);
-        ch.host2.begin_prob(part, op.r, op.q, op.r, 0);
+        const size_t u0 = u;
         do {
-          const Seg& sg = op.segs[u++];
-          ch.host2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale, sg.btile);
-          kdone += sg.k;
-        } while (u < op.segs.size() && (kdone < kcut || sp == nsplit - 1));
-        ch.host2.end_prob();
+          kdone += seg_k(u++);
+        } while (u < nseg && (kdone < kcut || sp == nsplit - 1));
+        emit(part, 0, u0, u);
         ch.comb3.terms.push_back({part, 1.0});
         ws += qr + (qr & 1);
       }
@@ -878,6 +953,9 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     ch.host1.finalize_tiles(0, getenv("SDMRG_P1_BY_PROBLEM") != nullptr);
     ch.host2.finalize_tiles(p2_octaves(), getenv("SDMRG_P2_BY_PROBLEM") != nullptr);
     ch.p2_one_body = use_one_body(ch.host2);
+    ch.fused.finalize();
+    tiles += (int64_t)ch.fused.tiles.size();
+    segments += (int64_t)ch.fused.segs.size();
     ch.ws_doubles = ws;
     tiles += (int64_t)(ch.host1.tiles.size() + ch.host2.tiles.size());
     segments += (int64_t)(ch.host1.segs.size() + ch.host2.segs.size());
@@ -975,12 +1053,13 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
                              "memset workspace");
   }
   if (!rc && !plan->chunks.empty())
-    rc = cuda_check(cudaMalloc(&plan->counters, sizeof(int) * 2 * plan->chunks.size()),
+    rc = cuda_check(cudaMalloc(&plan->counters, sizeof(int) * 3 * plan->chunks.size()),
                     "cudaMalloc counters");
   for (auto& ch : plan->chunks) {
     if (rc) break;
     rc = ch.host1.upload(&ch.p1, 0);
     if (!rc) rc = ch.host2.upload(&ch.p2, 0);
+    if (!rc) rc = ch.fused.upload();
     for (CombList* cl : {&ch.comb0, &ch.comb3}) {
       if (!rc) rc = upload_vec(cl->tasks, &cl->d_tasks);
       if (!rc) rc = upload_vec(cl->outs, &cl->d_outs);
@@ -1015,13 +1094,15 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   st.workspace_doubles = ws_max;
   int64_t kernels = 0;
   for (auto& ch : plan->chunks)
-    kernels += (ch.comb0.ntasks > 0) + (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0) +
+    kernels += (ch.comb0.ntasks > 0) + (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0) + (ch.fused.ntiles > 0) +
                (ch.comb3.ntasks > 0);
   st.kernels_per_apply = kernels;
   st.algo_bytes = static_cast<int64_t>(algo_bytes);
   st.products = products;
   st.combine_outputs = comb_outputs;
   st.combine_terms = comb_terms;
+  st.fused_outs = plan->fused_outs;
+  st.arena_bytes = 8 * (psize_l + psize_r);
   *out = plan;
   return SDMRG_OK;
 }
@@ -1078,7 +1159,7 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (rc) return rc;
   }
   if (plan->chunks.empty()) return SDMRG_OK;
-  rc = cuda_check(cudaMemsetAsync(plan->counters, 0, sizeof(int) * 2 * plan->chunks.size(), stream),
+  rc = cuda_check(cudaMemsetAsync(plan->counters, 0, sizeof(int) * 3 * plan->chunks.size(), stream),
                   "memset counters");
   if (rc) return rc;
   if (plan->psi_copy.n > 0) {
@@ -1121,13 +1202,15 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (plan->timing) cudaEventRecord(ch.ev[1], s0);
     if (fork) cudaEventRecord(plan->join, plan->side);
     if (plan->timing) cudaEventRecord(ch.ev[2], stream);
-    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 2 * c, stream, true);
+    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 3 * c, stream, true);
     if (rc) return rc;
     if (plan->timing) cudaEventRecord(ch.ev[3], stream);
     if (fork) cudaStreamWaitEvent(stream, plan->join, 0);
     if (plan->timing) cudaEventRecord(ch.ev[4], stream);
-    rc = launch_engine(false, false, ch.p2, bases, plan->counters + 2 * c + 1, stream, true,
+    rc = launch_engine(false, false, ch.p2, bases, plan->counters + 3 * c + 1, stream, true,
                        ch.p2_one_body);
+    if (rc) return rc;
+    rc = launch_fused(ch.fused, bases, plan->counters + 3 * c + 2, stream);
     if (rc) return rc;
     if (plan->timing) {
       cudaEventRecord(ch.ev[5], stream);
@@ -1191,6 +1274,7 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
   for (auto& ch : plan->chunks) {
     ch.p1.release();
     ch.p2.release();
+    ch.fused.release();
     ch.comb0.release();
     ch.comb3.release();
     for (auto& e : ch.ev)

@@ -59,3 +59,27 @@ int launch_engine(bool ta, bool tb, const DeviceBatch& b, const Bases& bases, in
                   cudaStream_t stream, bool bulk = false, bool one_body = false);
 
 }  // namespace sdmrg
+
+#include "fused.cuh"
+
+namespace sdmrg {
+
+// Host staging of the fused small-sector work list (fused.cuh): one σ
+// problem = products (FSeg) + column tiles of <= F_RT 8-blocks.
+struct FusedBatch {
+  std::vector<FTileRec> tiles;
+  std::vector<double> tile_cost;
+  std::vector<FSeg> segs;
+  FTileRec* d_tiles = nullptr;
+  FSeg* d_segs = nullptr;
+  int64_t ntiles = 0;
+  // σ problem at handle c (q x r, ld ldc) over segs [seg_begin, segs.size())
+  void add_problem(uint64_t c, int ldc, int q, int r, int beta, int32_t seg_begin);
+  void finalize();         // descending-cost order (LPT)
+  int upload();
+  void release();
+};
+int launch_fused(const FusedBatch& b, const Bases& bases, int* counter, cudaStream_t stream);
+int fused_grid_size();  // persistent fused-kernel grid on the current device
+
+}  // namespace sdmrg

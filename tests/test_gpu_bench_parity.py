@@ -29,13 +29,23 @@ def _need_cuda():
         pytest.skip("no CUDA device")
 
 
-def _check(n_orb, d, frac, seed, workspace_doubles=0):
+def _check(n_orb, d, frac, seed, workspace_doubles=0, n_elec=None, fused=None):
+    import os
     from oracle import heff
     from paper_2305_05581_b200.plan import DevicePlan
     from paper_2305_05581_b200.workload import fill_arenas_device, synthetic_plan_input
-    pi = synthetic_plan_input(n_orb, d, seed=seed)
+    pi = synthetic_plan_input(n_orb, d, seed=seed, n_elec=n_elec)
     al, ar = fill_arenas_device(pi, seed=seed)
-    plan = DevicePlan(pi, arena_l=al, arena_r=ar, workspace_doubles=workspace_doubles)
+    old = os.environ.get("SDMRG_FUSED")
+    if fused is not None:
+        os.environ["SDMRG_FUSED"] = "1" if fused else "0"
+    try:
+        plan = DevicePlan(pi, arena_l=al, arena_r=ar, workspace_doubles=workspace_doubles)
+    finally:
+        if old is None:
+            os.environ.pop("SDMRG_FUSED", None)
+        else:
+            os.environ["SDMRG_FUSED"] = old
     nk = plan.stats["psi_keys"]
     rng = np.random.default_rng(seed + 17)
     subset = np.sort(rng.choice(nk, size=max(1, int(np.ceil(frac * nk))), replace=False))
@@ -75,3 +85,17 @@ def test_sigma_subset_L30_D2048_multichunk():
 def test_sigma_subset_L50_D4096():
     stats, ng = _check(50, 4096, 0.10, seed=5)
     assert ng > 1000
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_sigma_subset_L30_D1024_paths(fused):
+    """The two-phase engine alone and the fused small-sector kernel (with the
+    two-phase engine for the sectors beyond 64) on the same subset."""
+    stats, ng = _check(30, 1024, 0.10, seed=6, fused=fused)
+    assert (stats["fused_outs"] > 0) == fused
+
+
+def test_sigma_subset_L76_D4096():
+    """CAS(113,76)-sized partition (north-star workload): fused kernel."""
+    stats, ng = _check(76, 4096, 0.03, seed=7, n_elec=113)
+    assert ng > 1000 and stats["fused_outs"] > 0

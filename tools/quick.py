@@ -4,13 +4,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
 from paper_2305_05581_b200.plan import DevicePlan
-from paper_2305_05581_b200.workload import fill_arenas_device, synthetic_plan_input
+from paper_2305_05581_b200.workload import fill_plan_arenas, synthetic_plan_input
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 D = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
-pi = synthetic_plan_input(L, D)
-al, ar = fill_arenas_device(pi)
+NE = int(sys.argv[3]) if len(sys.argv) > 3 else None   # electrons (L=76: 113)
+pi = synthetic_plan_input(L, D, n_elec=NE)
 ws = int(os.environ.get("SDMRG_WS", "0"))
-plan = DevicePlan(pi, arena_l=al, arena_r=ar, workspace_doubles=ws)
+plan = DevicePlan(pi, empty_arenas=True, workspace_doubles=ws)
+fill_plan_arenas(plan, pi)
 psi = torch.randn(plan.psi_size, dtype=torch.float64, device="cuda")
 out = plan.empty_vector()
 for _ in range(2):
