@@ -259,6 +259,40 @@ class Launch:
 
 # ---------------------------------------------------------- partial sums
 
+def _defs_prep(defs):
+    """Store-independent preprocessing of a definition set (the term keys,
+    the three-factor head/tail split), cached in ``defs`` — the driver
+    reuses one defs object per partition for the whole run."""
+    prep = defs.get("_prep")
+    if prep is not None:
+        return prep
+    aux, inside = defs["aux"], defs["inside"]
+    nf = (inside >= 0).sum(axis=1)
+
+    def op_key(codes):
+        f = decode(codes)
+        return ("C",) + f if len(f) == 1 else ("P",) + f
+
+    direct = np.nonzero(nf <= 2)[0]
+    three = np.nonzero(nf == 3)[0]
+    prep = {"direct": direct, "direct_keys": [op_key(inside[t]) for t in direct.tolist()],
+            "three": three}
+    if len(three):
+        heads = [("C",) + decode(inside[t][:1]) for t in three.tolist()]
+        tails = [("P",) + decode(inside[t][1:3]) for t in three.tolist()]
+        mkeys, mindex = [], {}
+        m_of = np.empty(len(three), np.int64)
+        for i, (t, h) in enumerate(zip(three.tolist(), heads)):
+            mk = (int(aux[t]), h)
+            if mk not in mindex:
+                mindex[mk] = len(mkeys)
+                mkeys.append(mk)
+            m_of[i] = mindex[mk]
+        prep.update(tails=tails, mkeys=mkeys, m_of=m_of)
+    defs["_prep"] = prep
+    return prep
+
+
 def composites(store, defs, model, device):
     """Σ_t coef_t · resolve(factors_t) for each definition (blocks.py:331
     materialize_aux / the cross sums of blocks.py:262).
@@ -269,43 +303,29 @@ def composites(store, defs, model, device):
     on the store basis holding the composites under their keys."""
     ops = store.ops
     out = ClassArena(ops.basis, [(d[0], d[1]) for d in defs["keys"]], device, zero=True)
-    aux, coef, inside = defs["aux"], defs["coef"], defs["inside"]
+    aux, coef = defs["aux"], defs["coef"]
     if len(aux) == 0:
         return out
-    nf = (inside >= 0).sum(axis=1)
+    prep = _defs_prep(defs)
     keys = [k for k, _ in defs["keys"]]
-
-    def op_key(codes):
-        f = decode(codes)
-        return ("C",) + f if len(f) == 1 else ("P",) + f
-
     # one- and two-factor strings: out_class = K @ store_class
-    direct = np.nonzero(nf <= 2)[0]
-    for t in direct.tolist():
-        if not ops.has(op_key(inside[t])):
-            raise KeyError(f"operator {op_key(inside[t])} not maintained on block {store.sites}")
-    _class_gemm(out, keys, ops, aux, coef, direct, [op_key(inside[t]) for t in direct.tolist()])
+    direct = prep["direct"]
+    for tk in prep["direct_keys"]:
+        if not ops.has(tk):
+            raise KeyError(f"operator {tk} not maintained on block {store.sites}")
+    _class_gemm(out, keys, ops, aux, coef, direct, prep["direct_keys"])
     # three-factor strings: M_(c, head) = Σ c · P (GEMM), out += Σ_head C · M
-    three = np.nonzero(nf == 3)[0]
+    three = prep["three"]
     if len(three):
-        heads = [("C",) + decode(inside[t][:1]) for t in three.tolist()]
-        tails = [("P",) + decode(inside[t][1:3]) for t in three.tolist()]
-        mkeys = []
-        mindex = {}
-        m_of = np.empty(len(three), np.int64)
-        for i, (t, h) in enumerate(zip(three.tolist(), heads)):
-            mk = (int(aux[t]), h)
-            if mk not in mindex:
-                mindex[mk] = len(mkeys)
-                mkeys.append(mk)
-            m_of[i] = mindex[mk]
+        mkeys = prep["mkeys"]
         mdeltas = []
         for (c, h) in mkeys:
             hd = ops.delta(h)
             cd = out.delta(keys[c])
             mdeltas.append(tuple(a - b for a, b in zip(cd, hd)))
         marena = ClassArena(ops.basis, [(mk, dl) for mk, dl in zip(mkeys, mdeltas)], device)
-        _class_gemm(marena, mkeys, ops, m_of, coef[three], np.arange(len(three)), tails)
+        _class_gemm(marena, mkeys, ops, prep["m_of"], coef[three], np.arange(len(three)),
+                    prep["tails"])
         _head_products(out, keys, ops, marena, mkeys)
     return out
 
@@ -315,21 +335,36 @@ def _class_gemm(out, out_keys, ops, aux, coef, terms, term_keys):
     GEMM per (output class, source class): C = K · S."""
     if len(terms) == 0:
         return
-    by_pair = {}
-    for t, tk in zip(np.asarray(terms).tolist(), term_keys):
-        cl_o, r_o = out.ops[out_keys[int(aux[t])]]
-        cl_s, r_s = ops.ops[tk]
-        if cl_o.delta != cl_s.delta:
-            raise ValueError(f"term {tk} shift {cl_s.delta} != composite shift {cl_o.delta}")
-        ent = by_pair.setdefault((id(cl_o), id(cl_s)), (cl_o, cl_s, {}))
-        ent[2][(r_o, r_s)] = ent[2].get((r_o, r_s), 0.0) + float(coef[t])
+    terms = np.asarray(terms)
+    outs = [out.ops[out_keys[a]] for a in np.asarray(aux)[terms].tolist()]
+    srcs = [ops.ops[tk] for tk in term_keys]
+    cls_ids = {}
+    cls = []
+
+    def cid(cl):
+        i = cls_ids.get(id(cl))
+        if i is None:
+            i = cls_ids[id(cl)] = len(cls)
+            cls.append(cl)
+        return i
+
+    co = np.array([cid(c) for c, _ in outs], np.int64)
+    ro = np.array([r for _, r in outs], np.int64)
+    cs = np.array([cid(c) for c, _ in srcs], np.int64)
+    rs = np.array([r for _, r in srcs], np.int64)
+    cf = np.asarray(coef, np.float64)[terms]
     dev = out.arena.device
-    for cl_o, cl_s, entries in by_pair.values():
+    pair = co * len(cls) + cs
+    order = np.argsort(pair, kind="stable")
+    bounds = np.nonzero(np.diff(pair[order]))[0] + 1
+    for grp in np.split(order, bounds):
+        cl_o, cl_s = cls[int(co[grp[0]])], cls[int(cs[grp[0]])]
+        if cl_o.delta != cl_s.delta:
+            raise ValueError(f"term shift {cl_s.delta} != composite shift {cl_o.delta}")
         if cl_o.size == 0:
             continue
         k = np.zeros((cl_o.nops, cl_s.nops))
-        for (r_o, r_s), v in entries.items():
-            k[r_o, r_s] += v
+        np.add.at(k, (ro[grp], rs[grp]), cf[grp])
         kd = torch.from_numpy(k).to(dev)
         ln = Launch(0, 0)
         ln.add(handle(0, cl_o.base), cl_o.size, cl_o.nops, cl_o.size, 0, 1,
@@ -337,49 +372,57 @@ def _class_gemm(out, out_keys, ops, aux, coef, terms, term_keys):
         ln.run([out.arena, kd, ops.arena])
 
 
+def _slot_table(cl, nsec):
+    t = getattr(cl, "_slots", None)
+    if t is None or len(t) != nsec:
+        t = np.full(nsec, -1, np.int64)
+        t[cl.col] = np.arange(len(cl.col))
+        cl._slots = t
+    return t
+
+
 def _head_products(out, keys, ops, marena, mkeys):
     """out[c] += Σ_head C_head · M_(c, head): per output block one problem,
     the heads its segments (blocks.py:104 resolve of 3-factor strings)."""
     basis = ops.basis
     dims = basis.dims
-    prob = {}
+    nsec = len(basis)
+    parts = []
     for mk in mkeys:
         c, h = mk
         cl_o, r_o = out.ops[keys[c]]
         cl_m, r_m = marena.ops[mk]
         cl_h, r_h = ops.ops[h]
-        for slot, j in enumerate(cl_o.col.tolist()):
-            ms = cl_m.col_pos.get(j)
-            if ms is None:
-                continue
-            jm = int(cl_m.row[ms])
-            hs = cl_h.col_pos.get(jm)
-            if hs is None:
-                continue
-            jr = int(cl_h.row[hs])
-            if jr != int(cl_o.row[slot]):
-                raise ValueError("selection rule mismatch in a three-factor product")
-            dst = cl_o.base + r_o * cl_o.size + int(cl_o.off[slot])
-            prob.setdefault(dst, (int(dims[jr]), int(dims[j]), []))[2].append(
-                (cl_h.base + r_h * cl_h.size + int(cl_h.off[hs]),
-                 cl_m.base + r_m * cl_m.size + int(cl_m.off[ms]), int(dims[jm])))
-    if not prob:
+        j = cl_o.col
+        if len(j) == 0:
+            continue
+        ms = _slot_table(cl_m, nsec)[j]
+        ok = ms >= 0
+        jm = np.where(ok, cl_m.row[np.maximum(ms, 0)], 0)
+        hs = np.where(ok, _slot_table(cl_h, nsec)[jm], -1)
+        ok &= hs >= 0
+        if not ok.any():
+            continue
+        slot = np.nonzero(ok)[0]
+        ms, hs, jm = ms[slot], hs[slot], jm[slot]
+        jr = cl_h.row[hs]
+        if np.any(jr != cl_o.row[slot]):
+            raise ValueError("selection rule mismatch in a three-factor product")
+        parts.append((cl_o.base + r_o * cl_o.size + cl_o.off[slot], dims[jr], dims[j[slot]],
+                      cl_h.base + r_h * cl_h.size + cl_h.off[hs],
+                      cl_m.base + r_m * cl_m.size + cl_m.off[ms], dims[jm]))
+    if not parts:
         return
+    dst, m, n, a, b, k = (np.concatenate([p[x] for p in parts]) for x in range(6))
+    order = np.argsort(dst, kind="stable")       # segments of a block in head order
+    dst, m, n, a, b, k = dst[order], m[order], n[order], a[order], b[order], k[order]
+    first = np.concatenate([[True], dst[1:] != dst[:-1]])
+    starts = np.nonzero(first)[0]
+    nseg = np.diff(np.concatenate([starts, [len(dst)]]))
     ln = Launch(0, 0)
-    cs, ms_, ns, nseg, a, b, lda, ldb, kk = [], [], [], [], [], [], [], [], []
-    for dst, (m, n, segs) in prob.items():
-        cs.append(dst)
-        ms_.append(m)
-        ns.append(n)
-        nseg.append(len(segs))
-        for ah, bh, k in segs:
-            a.append(ah)
-            b.append(bh)
-            lda.append(k)
-            ldb.append(n)
-            kk.append(k)
-    ln.add(handle(0, cs), ns, ms_, ns, np.ones(len(cs), np.int64), nseg,
-           handle(1, a), lda, handle(2, b), ldb, kk, np.ones(len(a)))
+    ln.add(handle(0, dst[starts]), n[starts], m[starts], n[starts],
+           np.ones(len(starts), np.int64), nseg,
+           handle(1, a), k, handle(2, b), n, k, np.ones(len(a)))
     ln.run([out.arena, ops.arena, marena.arena])
 
 

@@ -30,11 +30,11 @@
 //
 // Pipeline: the same warp-specialized ring as engine.cuh (1 producer warp,
 // 16-byte cp.async with mbarrier completion), stage kinds:
-//   STEP1  R_b[r-tile rows][32 n-cols] + ψ_i[8 mb rows][32 n-cols]
+//   STEP1  R_b[r-tile rows][64 n-cols] + ψ_i[8 mb rows][64 n-cols]
 //   COPY   ψ_i[8 mb rows][r-tile cols]            (identity R)
-//   LHALF  L[q rows][32 m-cols]  (one per 32 columns of m)
+//   LSTAGE L[q rows][m cols]  (m <= 64: one stage per product)
 // Zero fill: every k (n) tail, the ψ rows [m, 8 mb) and the L columns
-// [m, 32) of a half are zero-filled by the copies (so the padded T^T columns
+// [m, 64) are zero-filled by the copies (so the padded T^T columns
 // are exactly zero); rows of R beyond the tile and of L beyond q only feed
 // accumulator rows / columns the epilogue never stores.
 #pragma once
@@ -63,35 +63,39 @@ struct FSeg {         // 48 B: one (ψ key, right op) product of a σ problem
   double scale;
 };
 
-constexpr int FKC = 32;             // n columns per STEP1 stage
+constexpr int FKC = 64;             // n columns per STEP1 stage
 constexpr int FKLD = FKC + 2;       // K-contiguous row stride (≡ 2 mod 16: conflict-free LDS.64)
 constexpr int F_RT = 5;             // <= 5 column blocks per tile (40 σ columns)
 constexpr int F_QB = 8;             // q <= 64
 constexpr int F_MB = 8;             // m <= 64
-constexpr int FLLD = 32 + 8;        // L half row stride (≡ 8 mod 16: conflict-free LDS.128)
+constexpr int FLLD = 64 + 8;        // L stage row stride (≡ 8 mod 16: conflict-free LDS.128)
 constexpr int FCLD = 8 * F_RT + 10; // COPY row stride (≡ 2 mod 16)
 constexpr int F_A_EL = 8 * F_RT * FKLD;
 constexpr int F_STAGE_EL = F_A_EL + 8 * F_MB * FKLD;
-static_assert(8 * F_QB * FLLD <= F_STAGE_EL, "L half fits a stage");
+static_assert(8 * F_QB * FLLD <= F_STAGE_EL, "L stage fits a stage");
 static_assert(8 * F_MB * FCLD <= F_STAGE_EL, "COPY stage fits a stage");
 #ifndef SDMRG_FMINB
 #define SDMRG_FMINB 1
 #endif
 #ifndef SDMRG_FSTAGES
-#define SDMRG_FSTAGES 6
+#define SDMRG_FSTAGES 3
 #endif
 constexpr int FSTAGES = SDMRG_FSTAGES;
 constexpr int F_SLD = 8 * F_QB + 2;                   // reduction scratch row stride
 constexpr int F_SCRATCH_EL = 8 * F_RT * F_SLD;
-constexpr int F_THREADS = 32 * 5;
+#ifndef SDMRG_FPRODUCERS
+#define SDMRG_FPRODUCERS 4
+#endif
+constexpr int F_PRODUCERS = SDMRG_FPRODUCERS;
+constexpr int F_THREADS = 32 * (4 + F_PRODUCERS);
 
 struct FMeta {
   double* c;
   double scale;
-  int32_t type;      // 1 STEP1, 2 LHALF, 3 COPY
+  int32_t type;      // 1 STEP1, 2 LSTAGE, 3 COPY
   int32_t nks;       // STEP1: k4 steps in the stage
   int32_t mb;        // m blocks of the stage's product
-  int32_t half;      // LHALF: which 32 columns of m
+  int32_t half;      // unused
   int32_t flags;     // kFirst / kLast / kEnd / kSegEnd
   int32_t ldc, beta;
   int16_t q, rt;
@@ -131,6 +135,7 @@ __device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_
   const FMeta& first = reinterpret_cast<const FMeta*>(ring.meta)[stage];
   double* const cbase = first.c;
   const int ldc = first.ldc, beta = first.beta, q = first.q, rt = first.rt;
+  g = 0;  // per-tile deal: the result depends on the tile only (bitwise determinism)
   int j0 = (w - g) & 3;
   constexpr uint32_t STAGE_B = F_STAGE_EL * 8;
   while (true) {
@@ -182,11 +187,10 @@ __device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_
       }
     } else {
       // σ^T[8a + lr][8c + ·] += s T^T[8a + lr][8j + 2lc + e] L[8c + ·][8j + 2lc + e]
-      const int h = m.half;
       const double s = m.scale;
-      const uint32_t pl = sa + (lr * FLLD + 8 * j0 + 2 * lc) * 8;
       auto step2 = [&](auto h_t) {
         constexpr int H = decltype(h_t)::value;
+        const uint32_t pl = sa + (lr * FLLD + 8 * (j0 + 4 * H) + 2 * lc) * 8;
 #ifndef FX_NOSCALE
         if (__double_as_longlong(s) != 0x3FF0000000000000LL) {
 #pragma unroll
@@ -208,11 +212,8 @@ __device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_
         }
       };
 #ifndef FX_NOSTEP2
-      if (h == 0) {
-        if (v0) step2(std::integral_constant<int, 0>{});
-      } else {
-        if (v1) step2(std::integral_constant<int, 1>{});
-      }
+      if (v0) step2(std::integral_constant<int, 0>{});
+      if (v1) step2(std::integral_constant<int, 1>{});
 #endif
       if (flags & kSegEnd) {
 #pragma unroll
@@ -279,15 +280,20 @@ __device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_
   SDMRG_FCASE(RT, 5) SDMRG_FCASE(RT, 6) SDMRG_FCASE(RT, 7) SDMRG_FCASE(RT, 8)
 
 // ------------------------------------------------------------------ producer
-// 16-byte copies of `rows` rows x 32 K-columns starting at column k0 of a
-// row-major source (ld even, k0 even), zero-filling columns >= kvalid and
-// rows >= rvalid; destination row stride LD.
+// F_PRODUCERS warps share every stage's copies (row r -> warp r mod
+// F_PRODUCERS): one warp issuing ~50 cp.async per lane and stage could not
+// keep four DMMA warps fed (ncu r2d: 14% DMMA-pipe activity with a single
+// producer, consumers spinning on the full barriers).
+//
+// 16-byte copies of `rows` rows x 64 K-columns of a row-major source (ld
+// even, column offset even), zero-filling columns >= kvalid and rows >=
+// rvalid; destination row stride LD.
 template <int LD>
-__device__ __forceinline__ void f_load_rows32(uint32_t sdst, const double* src, int ld, int rows,
-                                              int rvalid, int kvalid, int lane) {
-  const int kp = lane & 15, k = 2 * kp;
+__device__ __forceinline__ void f_load_rows64(uint32_t sdst, const double* src, int ld, int rows,
+                                              int rvalid, int kvalid, int lane, int pw) {
+  const int k = 2 * lane;
   const int bytes = k + 1 < kvalid ? 16 : (k < kvalid ? 8 : 0);
-  for (int r = lane >> 4; r < rows; r += 2) {
+  for (int r = pw; r < rows; r += F_PRODUCERS) {
     const bool ok = r < rvalid && bytes > 0;
     cp_async16(sdst + (r * LD + k) * 8, ok ? src + (int64_t)r * ld + k : src, ok ? bytes : 0);
   }
@@ -296,27 +302,35 @@ __device__ __forceinline__ void f_load_rows32(uint32_t sdst, const double* src, 
 __device__ __forceinline__ void fused_produce(const Ring& ring, const FTileRec* __restrict__ tiles,
                                               int ntiles, const FSeg* __restrict__ segs,
                                               int* __restrict__ counter, double* const* sbases,
-                                              int lane) {
+                                              int lane, int pw, volatile int* s_tile) {
   FMeta* meta = reinterpret_cast<FMeta*>(ring.meta);
+  const bool lead = pw == 0 && lane == 0;
   int stage = 0;
   uint32_t phase = 0;
   auto open = [&]() { mbar_wait(ring.empty0 + 8 * stage, phase ^ 1); };
   auto close = [&]() {
     __syncwarp();
     mbar_arrive_cp_async(ring.full0 + 8 * stage);
-    if (lane == 0) mbar_arrive(ring.full0 + 8 * stage);
+    if (lead) mbar_arrive(ring.full0 + 8 * stage);
     if (++stage == FSTAGES) {
       stage = 0;
       phase ^= 1;
     }
   };
   auto res = [&](uint64_t h) { return sbases[h >> kHandleShift] + (h & kHandleMask); };
-  int t = 0;
-  if (lane == 0) t = atomicAdd(counter, 1);
-  t = __shfl_sync(0xffffffffu, t, 0);
+  // tile queue: the lead claims, the producer warps read it after a named
+  // barrier (slots alternate, so a slot is rewritten only after every warp
+  // has passed the next barrier)
+  int par = 0;
+  auto next_tile = [&]() {
+    if (lead) s_tile[par] = atomicAdd(counter, 1);
+    named_bar(2, 32 * F_PRODUCERS);
+    const int v = s_tile[par];
+    par ^= 1;
+    return v;
+  };
+  int t = next_tile();
   while (t < ntiles) {
-    int tn = 0;
-    if (lane == 0) tn = atomicAdd(counter, 1);
     const FTileRec tr = tiles[t];
     double* cptr = res(tr.c);
     bool first = true;
@@ -328,7 +342,7 @@ __device__ __forceinline__ void fused_produce(const Ring& ring, const FTileRec* 
       const bool last_seg = s + 1 == tr.seg_end;
       const double* psi = res(sg.psi);
       auto meta_write = [&](int type, int nks, int half, int flags) {
-        if (lane == 0) {
+        if (lead) {
           FMeta& mt = meta[stage];
           mt.type = type;
           mt.nks = nks;
@@ -353,8 +367,8 @@ __device__ __forceinline__ void fused_produce(const Ring& ring, const FTileRec* 
           const uint32_t st = ring.smem + stage * (F_STAGE_EL * 8);
           const int kv = n - c0;
           meta_write(1, (min(FKC, kv) + 3) >> 2, 0, 0);
-          f_load_rows32<FKLD>(st, rb + c0, pad2d(n), tr.rt, tr.rt, kv, lane);
-          f_load_rows32<FKLD>(st + F_A_EL * 8, psi + c0, pad2d(n), 8 * mb, m, kv, lane);
+          f_load_rows64<FKLD>(st, rb + c0, pad2d(n), tr.rt, tr.rt, kv, lane, pw);
+          f_load_rows64<FKLD>(st + F_A_EL * 8, psi + c0, pad2d(n), 8 * mb, m, kv, lane, pw);
           close();
         }
       } else {
@@ -365,7 +379,7 @@ __device__ __forceinline__ void fused_produce(const Ring& ring, const FTileRec* 
         // keeps an odd last pair in bounds), rows >= m zero
         const int npair = (tr.rt + 1) >> 1;
         const double* p0 = psi + tr.r0;
-        for (int x = lane; x < 8 * mb * npair; x += 32) {
+        for (int x = lane + 32 * pw; x < 8 * mb * npair; x += 32 * F_PRODUCERS) {
           const int r = x / npair, cp = x - r * npair;
           const bool ok = r < m;
           cp_async16(st + (r * FCLD + 2 * cp) * 8, ok ? p0 + (int64_t)r * pad2d(n) + 2 * cp : p0,
@@ -374,19 +388,16 @@ __device__ __forceinline__ void fused_produce(const Ring& ring, const FTileRec* 
         close();
       }
       const double* l = res(sg.l);
-      for (int h = 0; 32 * h < m; ++h) {
-        open();
-        const uint32_t st = ring.smem + stage * (F_STAGE_EL * 8);
-        const bool seg_end = 32 * (h + 1) >= m;
-        meta_write(2, 0, h, (seg_end ? kSegEnd : 0) | (seg_end && last_seg ? kLast : 0));
-        f_load_rows32<FLLD>(st, l + 32 * h, pad2d(m), tr.q, tr.q, m - 32 * h, lane);
-        close();
-      }
+      open();
+      const uint32_t st = ring.smem + stage * (F_STAGE_EL * 8);
+      meta_write(2, 0, 0, kSegEnd | (last_seg ? kLast : 0));
+      f_load_rows64<FLLD>(st, l, pad2d(m), tr.q, tr.q, m, lane, pw);
+      close();
     }
-    t = __shfl_sync(0xffffffffu, tn, 0);
+    t = next_tile();
   }
   open();
-  if (lane == 0) meta[stage].flags = kEnd;
+  if (lead) meta[stage].flags = kEnd;
   close();
 }
 
@@ -399,6 +410,7 @@ fused_heff_kernel(const FTileRec* __restrict__ tiles, int ntiles, const FSeg* __
   FMeta* meta = reinterpret_cast<FMeta*>(scratch + F_SCRATCH_EL);
   uint64_t* bars = reinterpret_cast<uint64_t*>(meta + FSTAGES);
   double** sbases = reinterpret_cast<double**>(bars + 2 * FSTAGES);
+  volatile int* s_tile = reinterpret_cast<volatile int*>(sbases + kMaxBases);
   Ring ring;
   ring.smem = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   ring.full0 = static_cast<uint32_t>(__cvta_generic_to_shared(bars));
@@ -409,18 +421,18 @@ fused_heff_kernel(const FTileRec* __restrict__ tiles, int ntiles, const FSeg* __
 #pragma unroll
     for (int k = 0; k < kMaxBases; ++k) sbases[k] = bases.p[k];
     for (int s = 0; s < FSTAGES; ++s) {
-      mbar_init(ring.full0 + 8 * s, 32 + 1);
+      mbar_init(ring.full0 + 8 * s, 32 * F_PRODUCERS + 1);
       mbar_init(ring.empty0 + 8 * s, 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (warp == 4) {
-    fused_produce(ring, tiles, ntiles, segs, counter, sbases, lane);
+  if (warp >= 4) {
+    fused_produce(ring, tiles, ntiles, segs, counter, sbases, lane, warp - 4, s_tile);
     return;
   }
   const int w = warp;
-  int stage = 0, g = static_cast<int>(blockIdx.x) & 3;
+  int stage = 0, g = 0;
   uint32_t phase = 0;
   while (true) {
     mbar_wait(ring.full0 + 8 * stage, phase);

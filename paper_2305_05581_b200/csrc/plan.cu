@@ -600,7 +600,12 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   for (int64_t i = 0; i < nk; ++i) total_t += t_need[i];
   int64_t budget = d->workspace_doubles;
   if (budget <= 0 && !d->dry_run) {
-    const double avail = (double)free_b - (plan->lsum_persistent ? 8.0 * total_l : 0.0);
+    // what the plan allocates besides the workspace: padded arenas (unless
+    // the caller already holds them: empty_arenas), padded ψ, pre-sums
+    const double own = 8.0 * ((double)psize_l + (double)psize_r + (double)plan->poffs[nk] +
+                              (plan->tiled ? (double)plan->ptoffs[nk] : 0.0));
+    const double avail = std::max(0.0, (double)free_b - own -
+                                  (plan->lsum_persistent ? 8.0 * total_l : 0.0));
     budget = std::max<int64_t>(1 << 20, (int64_t)(avail / 8 * 0.30));
   }
   int64_t max_key = 0;

@@ -632,19 +632,98 @@ def plan_input(model, table, comp_tab, left, right, comp_l, comp_r, target, devi
     return pi, sides["l"][0], sides["r"][0]
 
 
+_AUX_DEFS = {}
+
+
 def aux_defs(model, aux):
     """AuxDefs of one side as composite definitions keyed like the table's
-    ("AUX", side, factors) operator keys."""
+    ("AUX", side, factors) operator keys (memoized per AuxDefs object: the
+    tables are cached per position, so one defs object serves every visit
+    and carries its term preprocessing, blockops._defs_prep)."""
+    hit = _AUX_DEFS.get(id(aux))
+    if hit is not None and hit[0] is aux:
+        return hit[1]
     keys = []
     for a in range(len(aux.keys)):
         first = np.nonzero(aux.aux == a)[0][0]
         keys.append((("AUX", aux.side, aux.key_tuple(a)),
                      model.factor_delta(decode(aux.inside[first]))))
-    return {"keys": keys, "aux": aux.aux.astype(np.int64), "coef": aux.coef,
+    defs = {"keys": keys, "aux": aux.aux.astype(np.int64), "coef": aux.coef,
             "inside": aux.inside.astype(np.int64)}
+    if len(_AUX_DEFS) > 256:
+        _AUX_DEFS.clear()
+    _AUX_DEFS[id(aux)] = (aux, defs)
+    return defs
 
 
 # ------------------------------------------------------------------ driver
+
+def _store_tensors(store):
+    ts = [store.ops.arena]
+    if store.transform:
+        ts += list(store.transform.values())
+    return ts
+
+
+def store_bytes(store):
+    return sum(t.numel() * t.element_size() for t in _store_tensors(store))
+
+
+def _move_store(store, device):
+    store.ops.arena = store.ops.arena.to(device)
+    if store.transform:
+        store.transform = {k: v.to(device) for k, v in store.transform.items()}
+
+
+class StoreDict(dict):
+    """Block stores of one side by site count, resident in HBM up to a byte
+    budget (default 35% of the device's memory): the least recently used
+    stores beyond it wait in host memory and come back on access.  A sweep
+    touches one store per side and step, so at L=30 D=2048 (2.5 GB per
+    store, 2 x 28 of them) only the stores around the sweep position stay on
+    the device."""
+
+    def __init__(self, device=None, budget=None):
+        super().__init__()
+        self.device = device
+        if budget is None and device is not None and device.type == "cuda":
+            budget = int(0.35 * torch.cuda.get_device_properties(device).total_memory)
+        self.budget = budget
+        self.order = []          # keys, least recently used first
+        self.offloads = 0
+
+    def _touch(self, key):
+        if key in self.order:
+            self.order.remove(key)
+        self.order.append(key)
+
+    def _trim(self):
+        if self.budget is None:
+            return
+        resident = [k for k in self.order
+                    if dict.__getitem__(self, k).ops.arena.device.type == "cuda"]
+        total = sum(store_bytes(dict.__getitem__(self, k)) for k in resident)
+        for k in resident[:-2]:            # the two most recent always stay
+            if total <= self.budget:
+                break
+            st = dict.__getitem__(self, k)
+            total -= store_bytes(st)
+            _move_store(st, "cpu")
+            self.offloads += 1
+
+    def __getitem__(self, key):
+        st = dict.__getitem__(self, key)
+        if self.device is not None and st.ops.arena.device != self.device:
+            _move_store(st, self.device)
+        self._touch(key)
+        self._trim()
+        return st
+
+    def __setitem__(self, key, st):
+        dict.__setitem__(self, key, st)
+        self._touch(key)
+        self._trim()
+
 
 @dataclass
 class DmrgState:
@@ -655,8 +734,8 @@ class DmrgState:
     seed: int
     rng: object
     engine: object
-    left: dict = field(default_factory=dict)
-    right: dict = field(default_factory=dict)
+    left: dict = field(default_factory=StoreDict)
+    right: dict = field(default_factory=StoreDict)
     psi: object = None
     position: int = 0
     sweeps_done: int = 0
@@ -796,7 +875,8 @@ def warmup(model, schedule, target=None, seed=42, engine=None):
     engine = engine or Engine()
     dev = engine.device
     target = tuple(target) if target is not None else model.default_target()
-    state = DmrgState(model, target, seed, np.random.default_rng(seed), engine)
+    state = DmrgState(model, target, seed, np.random.default_rng(seed), engine,
+                      left=StoreDict(dev), right=StoreDict(dev))
     d = schedule.d_for(1)
     lo, hi = sweep_positions(model)
     n = model.n_sites
