@@ -49,9 +49,14 @@ def parse():
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--scale", default="30:2048",
-                    help="comma list of L:D workloads also timed at N=1 (configs[1] L=30 "
-                         "D=2048 by default; reported under 'scale_points'); empty to skip")
+    ap.add_argument("--scale", default="30:2048,76:4096:113",
+                    help="comma list of L:D[:electrons] workloads also timed at N=1 "
+                         "(configs[1] L=30 D=2048 and the north-star CAS(113,76) D=4096 by "
+                         "default; reported under 'scale_points'); empty to skip")
+    ap.add_argument("--sweep", default="16:256:1",
+                    help="L:D:sweeps of the closed-loop device DMRG timed at N=1 (BASELINE "
+                         "configs[0]: L=16 D=256; warm-up + SWEEPS timed sweeps, "
+                         "reported under 'sweep'); empty to skip")
     return ap.parse_args()
 
 
@@ -252,7 +257,8 @@ def scale_point(n_orb, d, seed, peak, applies=3, n_elec=None):
            "D": d, "ms_per_step": best, "ref_tflops": st["ref_flops"] / (best * 1e-3) / 1e12,
            "exec_tflops": st["exec_flops"] / (best * 1e-3) / 1e12,
            "exec_frac_of_dgemm": (st["exec_flops"] / (best * 1e-3) / 1e12) / peak if peak else None,
-           "chunks": st["chunks"], "psi_size": st["psi_size"],
+           "chunks": st["chunks"], "psi_size": st["psi_size"], "fused_outs": st["fused_outs"],
+           "n_elec": n_elec,
            "worklist": {"products": st["products"], "t_problems": st["t_problems"],
                         "tiles": st["tiles"], "segments": st["segments"],
                         "exec_mflop_per_tile": st["exec_flops"] / max(st["tiles"], 1) / 1e6}}
@@ -260,6 +266,48 @@ def scale_point(n_orb, d, seed, peak, applies=3, n_elec=None):
     del plan, psi, out
     torch.cuda.empty_cache()
     return res
+
+
+def sweep_point(n_orb, d, sweeps):
+    """sec/sweep of the closed-loop device DMRG (paper_2305_05581_b200.driver:
+    native factorization, device block stores, composites, H_eff·psi plans,
+    device Lanczos, renormalization, prediction) on the configs[0] model
+    (random integrals, model seed 16, run seed 42, Lanczos tol 1e-10 — the
+    run recorded from the reference in tests/golden/sweep_record_L16_D256.jsonl).
+    Wall clock around whole sweeps with a device synchronize on both sides;
+    per-stage times are the driver's own host timers (synchronized)."""
+    import torch
+    from paper_2305_05581_b200 import driver as drv
+    from paper_2305_05581_b200 import model as M
+    mm = M.Model(M.random_integrals(n_orb, 16, scale=0.2, core=0.3))
+    sch = drv.SweepSchedule(n_sweeps=sweeps, d=d, lanczos_tol=1e-10, lanczos_max_iter=300)
+    t0 = time.perf_counter()
+    st = drv.warmup(mm, sch, seed=42)
+    torch.cuda.synchronize()
+    warm = time.perf_counter() - t0
+    per = []
+    n0 = len(st.records)
+    for s in range(1, sweeps + 1):
+        t1 = time.perf_counter()
+        lo, hi = drv.sweep_positions(mm)
+        for p in range(lo, hi + 1):
+            drv._iterate(st, p, d, sch, s, "R")
+        for p in range(hi, lo - 1, -1):
+            drv._iterate(st, p, d, sch, s, "L")
+        st.sweeps_done = s
+        torch.cuda.synchronize()
+        per.append(time.perf_counter() - t1)
+    recs = st.records[n0:]
+    brk = {k: round(sum(r.timing.get(k, 0.0) for r in recs) / sweeps, 3)
+           for k in ("table_s", "aux_s", "plan_s", "lanczos_s", "renorm_s", "predict_s")}
+    return {"workload": f"closed-loop two-site DMRG, random-integral L={n_orb}, U(1)xU(1), "
+                        f"D={d} (BASELINE configs[0])",
+            "L": n_orb, "D": d, "sweeps": sweeps, "sec_per_sweep": per,
+            "warmup_s": round(warm, 3), "iterations_per_sweep": len(recs) // max(sweeps, 1),
+            "lanczos_iterations": sum(r.lanczos_iterations for r in recs),
+            "breakdown_s_per_sweep": brk,
+            "sweep_final_energy": recs[-1].energy if recs else None,
+            "store_offloads": st.left.offloads + st.right.offloads}
 
 
 def host_arenas(pi, seed):
@@ -360,9 +408,18 @@ def run_b200(args):
 
     peak = dgemm_peak(torch) if rank == 0 else None
     pi = synthetic_plan_input(args.L, args.D, seed=args.seed)
-    al, ar = fill_arenas_device(pi, seed=args.seed)
     t0 = time.perf_counter()
-    plan = DevicePlan(pi, arena_l=al, arena_r=ar, rank=rank, world=world)
+    if world == 1:
+        al, ar = fill_arenas_device(pi, seed=args.seed)
+        t0 = time.perf_counter()
+        plan = DevicePlan(pi, arena_l=al, arena_r=ar, rank=rank, world=world)
+    else:
+        # each rank holds only the operator blocks its ψ sectors read (left
+        # column sectors are sharded whole): generated in place, no dense copy
+        from paper_2305_05581_b200.workload import fill_plan_arenas
+        al = ar = None
+        plan = DevicePlan(pi, empty_arenas=True, rank=rank, world=world)
+        fill_plan_arenas(plan, pi, seed=args.seed)
     build_s = time.perf_counter() - t0
     st = plan.stats
     g = torch.Generator(device="cuda").manual_seed(args.seed + 1)
@@ -407,6 +464,10 @@ def run_b200(args):
     if world > 1:
         dist.all_reduce(ex)
     exec_total = float(ex.item())
+    ab = torch.tensor([float(st["arena_bytes"])], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ab, op=dist.ReduceOp.MAX)
+    arena_gb_max = float(ab.item()) / 1e9
 
     # dominant-kernel roofline: per-launch CUDA events inside the plan
     plan.set_timing(True)
@@ -495,15 +556,21 @@ def run_b200(args):
         al = ar = None
         torch.cuda.empty_cache()
         for item in [x for x in args.scale.split(",") if x.strip()]:
-            n_orb, d = (int(v) for v in item.split(":"))
-            scale.append(scale_point(n_orb, d, args.seed, peak))
+            v = [int(x) for x in item.split(":")]
+            scale.append(scale_point(v[0], v[1], args.seed, peak,
+                                     n_elec=v[2] if len(v) > 2 else None))
+    sweep = None
+    if world == 1 and args.sweep:
+        sweep = sweep_point(*[int(x) for x in args.sweep.split(":")])
 
     value = exec_total / (ms * 1e-3) / 1e12
     dom = 1 if phase_ms[1] >= phase_ms[2] else 2   # the tensor-bound engine phases
     if max(phase_ms[0], phase_ms[3]) > phase_ms[dom]:
         dom = 0 if phase_ms[0] >= phase_ms[3] else 3
     names = ["combine_kernel (phase 0: Lsum = sum s L)", "seg_gemm_kernel<0,1> (phase 1: T = A R^T)",
-             "seg_gemm_kernel<0,0> (phase 2: sigma += Lsum T)",
+             ("seg_gemm_kernel<0,0> + fused_heff_kernel (phase 2: sigma += Lsum T; fused "
+              "small-sector sigma problems)" if st.get("fused_outs") else
+              "seg_gemm_kernel<0,0> (phase 2: sigma += Lsum T)"),
              "combine_kernel (phase 3: split-K partials into sigma)"]
     if dom in (0, 3):
         achieved = phase_bytes[dom] / (phase_ms[dom] * 1e-3) / 1e9
@@ -531,6 +598,8 @@ def run_b200(args):
                    "l2": "inputs larger than L2 (operator arenas 2x%.1f GB)" % (
                        pi.meta["arena_size_l"] * 8 / 1e9),
                    "psi_size": st["psi_size"], "psi_keys": st["psi_keys"],
+                   "operator_arena_gb_per_rank_max": round(arena_gb_max, 2),
+                   "fused_sigma_problems_rank0": st["fused_outs"],
                    "groups": st["groups"], "members": st["members"],
                    "value_basis": "FP64 FLOPs the engine executes per H_eff·psi (all "
                                   "ranks) per device second: the sustained FP64 rate. "
@@ -554,6 +623,7 @@ def run_b200(args):
         "scale_points": scale,
         "e2e": e2e,
         "krylov": krylov,
+        "sweep": sweep,
         "gpu_launches": int(launches),
         "clocks": clk,
     }

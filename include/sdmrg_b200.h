@@ -185,6 +185,7 @@ typedef struct sdmrg_plan_stats {
   int64_t fused_outs;              /* σ problems on the fused small-sector    */
                                    /* kernel (T chained in registers)         */
   int64_t arena_bytes;             /* padded operator arenas held by the plan */
+  int64_t shard_balance_ppm;       /* mean / max rank cost x 1e6 (world > 1)  */
 } sdmrg_plan_stats;
 
 int sdmrg_plan_build(const sdmrg_plan_desc* desc, sdmrg_plan** out);

@@ -59,7 +59,7 @@ class PlanStats(ctypes.Structure):
         "local_members", "t_problems", "tiles", "segments", "chunks",
         "workspace_doubles", "kernels_per_apply", "algo_bytes", "products",
         "combine_outputs", "combine_terms", "build_ms_taskgen", "build_ms_emit",
-        "build_ms_device", "fused_outs", "arena_bytes")]
+        "build_ms_device", "fused_outs", "arena_bytes", "shard_balance_ppm")]
 
     def as_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

@@ -174,7 +174,15 @@ constexpr int WGRID_R = 2, WGRID_C = SDMRG_WIDE ? 4 : 2, CONSUMERS = WGRID_R * W
 constexpr int PRODUCERS = SDMRG_PRODUCERS;
 static_assert(PRODUCERS == 1 || PRODUCERS == 2, "one or two producer warps");
 constexpr int THREADS = 32 * (CONSUMERS + PRODUCERS);
-constexpr int KC_LD = BK + 2;                    // K-contiguous row stride (144 B)
+// SDMRG_SWZ: K-contiguous tiles unpadded ([64][16], 128-byte rows) with the
+// k4 groups of row r XOR-swizzled by (r & 3): element (r, k) at
+// r * 16 + (k ^ 4 (r & 3)).  A DMMA fragment load (rows lr, k lc of one k4
+// step) then hits 16 distinct bank pairs per half-warp; the padded stride 18
+// maps rows lr and lr + 1 two bank pairs apart (2-way conflicts for lc >= 2).
+#ifndef SDMRG_SWZ
+#define SDMRG_SWZ 0
+#endif
+constexpr int KC_LD = SDMRG_SWZ ? BK : BK + 2;   // K-contiguous row stride
 constexpr int NC_LD_A = BM + 4;                  // M-contiguous A row stride
 constexpr int NC_LD_B = BN + 4;                  // N-contiguous B row stride
 template <bool TA>
@@ -220,6 +228,7 @@ __host__ __device__ constexpr bool pack_path() {
   return SDMRG_PACK && (TB || SDMRG_PACK_P2);
 }
 static_assert(!(SDMRG_PACK && (SDMRG_LDS128 || SDMRG_DB)), "packing needs the natural k order");
+static_assert(!(SDMRG_SWZ && (SDMRG_PACK || SDMRG_LDS128 || SDMRG_DB)), "swizzle: natural-order bodies only");
 
 template <bool TA, bool TB>
 __host__ __device__ constexpr int smem_bytes() {
@@ -318,6 +327,15 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
   constexpr int B_J = TB ? 8 * KC_LD * 8 : 8 * 8;         // next 8-col block
   constexpr int A_KS = TA ? 4 * NC_LD_A * 8 : 4 * 8;      // next k4 step
   constexpr int B_KS = TB ? 4 * 8 : 4 * NC_LD_B * 8;
+  // swizzled K-contiguous operands: k4 step ks of row block sits at k4 group
+  // ks ^ (lr & 3) (a0 / b0 then point at k = lc of group 0)
+  const uint32_t sw = SDMRG_SWZ ? static_cast<uint32_t>((lane >> 2) & 3) : 0u;
+  auto koff_a = [&](int ks) -> uint32_t {
+    return (SDMRG_SWZ && !TA) ? ((static_cast<uint32_t>(ks) ^ sw) << 5) : uint32_t(ks * A_KS);
+  };
+  auto koff_b = [&](int ks) -> uint32_t {
+    return (SDMRG_SWZ && TB) ? ((static_cast<uint32_t>(ks) ^ sw) << 5) : uint32_t(ks * B_KS);
+  };
   double acc[MB > 0 ? MB : 1][NB > 0 ? NB : 1][2];
 #pragma unroll
   for (int i = 0; i < MB; ++i)
@@ -437,9 +455,9 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
           if (ks < nks) {
             double af[MB > 0 ? MB : 1], bf[NB > 0 ? NB : 1];
 #pragma unroll
-            for (int i = 0; i < MB; ++i) af[i] = lds64(a0 + ks * A_KS + i * A_I);
+            for (int i = 0; i < MB; ++i) af[i] = lds64(a0 + koff_a(ks) + i * A_I);
 #pragma unroll
-            for (int j = 0; j < NB; ++j) bf[j] = lds64(b0 + ks * B_KS + j * B_J);
+            for (int j = 0; j < NB; ++j) bf[j] = lds64(b0 + koff_b(ks) + j * B_J);
             if (SCALED) {
               const double sk = ksc(ks);
               if (NB <= MB) {
@@ -589,15 +607,17 @@ __device__ __forceinline__ void load_operand_async(uint32_t sbase, const double*
   if (KCONTIG) {
     const int kk = lane & 15, r0 = lane >> 4;
     const double* p = src + (int64_t)r0 * ld + kk;
-    const uint32_t s0 = sbase + (r0 * KC_LD + kk) * 8;
+    // swizzle: rows r0 + 2i alternate (r & 3) between r0 and r0 + 2
+    const int ke = SDMRG_SWZ ? kk ^ (4 * r0) : kk, ko = SDMRG_SWZ ? kk ^ (4 * (r0 + 2)) : kk;
+    const uint32_t se = sbase + (r0 * KC_LD + ke) * 8, so = sbase + (r0 * KC_LD + ko) * 8;
     const int nrow = (extent - r0 + 1) >> 1;
     if (kk < krem) {
 #pragma unroll 8
       for (int i = 0; i < nrow; ++i)
-        cp_async8_full(s0 + i * (2 * KC_LD * 8), p + (int64_t)(2 * i) * ld);
+        cp_async8_full((i & 1 ? so : se) + i * (2 * KC_LD * 8), p + (int64_t)(2 * i) * ld);
     } else {
 #pragma unroll 8
-      for (int i = 0; i < nrow; ++i) cp_async8(s0 + i * (2 * KC_LD * 8), src, false);
+      for (int i = 0; i < nrow; ++i) cp_async8((i & 1 ? so : se) + i * (2 * KC_LD * 8), src, false);
     }
   } else {
 #pragma unroll
@@ -640,7 +660,8 @@ __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const doubl
   if (KCONTIG) {
     const int k = 2 * (lane & 7), r0 = lane >> 3;
     const double* p = src + (int64_t)r0 * ld + k;
-    const uint32_t s0 = sbase + (r0 * KC_LD + k) * 8;
+    // rows r0 + 4i share (r & 3) = r0 & 3: one swizzled column per lane
+    const uint32_t s0 = sbase + (r0 * KC_LD + (SDMRG_SWZ ? k ^ (4 * (r0 & 3)) : k)) * 8;
     const int nrow = (extent - r0 + 3) >> 2;
     if (k + 1 < krem) {
 #pragma unroll 4

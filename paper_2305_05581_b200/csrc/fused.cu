@@ -15,19 +15,20 @@ namespace sdmrg {
 void FusedBatch::add_problem(uint64_t c, int ldc, int q, int r, int beta, int32_t seg_begin) {
   const int32_t seg_end = static_cast<int32_t>(segs.size());
   if (seg_end <= seg_begin) return;
-  // columns in balanced tiles of <= F_RT 8-blocks (e.g. 7 blocks -> 4 + 3)
-  const int rb = (r + 7) / 8;
-  const int nt = (rb + F_RT - 1) / F_RT;
-  const int per = 8 * ((rb + nt - 1) / nt);
-  double kcost = 0.0;  // DMMA work per 8-column block of the tile
+  // DMMA work of the problem per 8-column block of σ (step 1 + step 2)
   const int qb = (q + 7) / 8;
+  double kcost = 0.0;
   for (int s = seg_begin; s < seg_end; ++s) {
     const FSeg& sg = segs[s];
     const int mb = (sg.m + 7) / 8;
     kcost += double(mb) * (sg.ident ? 1.0 : (sg.n + 3) / 4) + double(mb) * 2.0 * qb;
   }
-  for (int r0 = 0; r0 < r; r0 += per) {
-    const int rt = std::min(per, r - r0);
+  // column tiles of 4 blocks, the remainder as 2 + 1 (fused_tile_blocks):
+  // every tile keeps the CTA's four DMMA warps busy
+  const int rb = (r + 7) / 8;
+  for (int b0 = 0; b0 < rb;) {
+    const int w = fused_tile_blocks(rb - b0);
+    const int r0 = 8 * b0, rt = std::min(8 * w, r - r0);
     FTileRec t{};
     t.c = c + static_cast<uint64_t>(r0);
     t.ldc = ldc;
@@ -38,7 +39,8 @@ void FusedBatch::add_problem(uint64_t c, int ldc, int q, int r, int beta, int32_
     t.rt = static_cast<int16_t>(rt);
     t.r0 = r0;
     tiles.push_back(t);
-    tile_cost.push_back(kcost * ((rt + 7) / 8) + 64.0);
+    tile_cost.push_back(kcost * w / 4.0 * 4.0 + 64.0);  // per-warp work: the tile's blocks / 4 warps
+    b0 += w;
   }
 }
 

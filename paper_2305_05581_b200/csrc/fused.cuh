@@ -5,36 +5,39 @@
 //     T(i, b)  = ψ_i R_b^T                      (phase 1, m x r, to HBM)
 //     σ_o     += Σ_(i, b) s · L(g, b) T(i, b)    (phase 2, reads T back)
 // and T is written and re-read once per use: at L=76 D=4096 that is 150 GB
-// of T per H_eff·ψ against 1.4 TFLOP of phase-2 math (tools: each T block is
-// used by ~1.1 groups), so the two-phase path is HBM-bound on small sectors.
+// of T per H_eff·ψ against 1.4 TFLOP of phase-2 math (each T block is used
+// by ~1.1 groups), so the two-phase path streams ~500 GB on small sectors.
 // This kernel evaluates the same sum per σ tile in the transposed form
 //     σ_o^T[r-tile, :] += Σ  (R_b[r-tile, :] ψ_i^T) · (s L^T)
-// chained in registers: a warp computes T^T = R_b ψ_i^T for an 8-column block
-// j of T^T (8 ψ rows) into DMMA accumulators, and those accumulators ARE the
-// A fragments of the second product (DMMA C layout: lane holds
-// T^T[row lr][cols 2lc, 2lc+1]; taking the k order of a k4 step as the
-// column pair (8j + 2lc + e, e = 0/1) makes element e of every accumulator
-// the A fragment of step e), so T exists only as 2 x RT registers per block.
-// The B fragments of the second product are L[q][8j + 2lc + e] — one
-// 16-byte shared load gives both steps.
+// chained in registers: a warp computes T^T = R_b ψ_i^T for its 8 rows of
+// the r-tile (8 σ columns) and the 8-column blocks j of m it owns into DMMA
+// accumulators, and those accumulators ARE the A fragments of the second
+// product (DMMA C layout: lane holds T^T[row lr][cols 2lc, 2lc+1]; taking the
+// k order of a k4 step as the column pair (8j + 2lc + e, e = 0/1) makes
+// element e of every accumulator the A fragment of step e).  The B fragments
+// of the second product are L[q][8j + 2lc + e] — one 16-byte shared load
+// gives both steps.
 //
-// Work split: a CTA owns one σ tile (all q rows, an r-range of <= 40
-// columns = RT 8-blocks) and walks its products (the concatenated K of
-// SBMM4S, sbmm4s.py:132-165).  The 8-row blocks j of each product's m
-// dimension are dealt round-robin to the 4 DMMA warps, continuing across
-// products, so the warps stay balanced whatever the sector sizes; each warp
-// accumulates a full σ^T tile (RT x QB blocks) and the four partial tiles
-// are summed in a fixed order at the tile's end (deterministic, no atomics).
-// Identity right operators (T = ψ_i) skip the first product: the A
-// fragments are read straight from a staged ψ block.
+// Work split (CTA = 4 DMMA warps + 2 producer warps, 2 CTAs per SM): a tile
+// is one σ problem's q rows x R = 4, 2 or 1 column blocks (r is cut
+// 4 + 4 + ... + 2 + 1).  Warp w owns column block w / S of the tile, S = 4 / R,
+// and of each product the m blocks j with (j + g) mod S == w mod S (g: the
+// tile's running block count, so the deal rotates across products).  R = 4:
+// every warp owns all of m and its own σ^T rows — no reduction; R = 2 / 1:
+// the S warps of a column block sum their partial σ^T in a fixed order at
+// the tile's end (deterministic, no atomics).  Accumulators per thread:
+// σ^T QB x 2 and T^T (8 / S) x 2 doubles — small enough for 2 CTAs (8 DMMA
+// warps) per SM: one DMMA warp per sub-partition cannot keep its FP64 pipe
+// busy (ncu r2f of the one-CTA variant: 29% DMMA-pipe activity, the stall
+// on the NOP that follows each DMMA).
 //
-// Pipeline: the same warp-specialized ring as engine.cuh (1 producer warp,
-// 16-byte cp.async with mbarrier completion), stage kinds:
-//   STEP1  R_b[r-tile rows][64 n-cols] + ψ_i[8 mb rows][64 n-cols]
-//   COPY   ψ_i[8 mb rows][r-tile cols]            (identity R)
-//   LSTAGE L[q rows][m cols]  (m <= 64: one stage per product)
+// Pipeline: the warp-specialized ring of engine.cuh (16-byte cp.async with
+// mbarrier completion), stage kinds:
+//   STEP1  R_b[8R rows][32 n-cols] + ψ_i[8 mb rows][32 n-cols]
+//   COPY   ψ_i[8 mb rows][r-tile cols]            (identity R: T = ψ_i)
+//   LHALF  L[q rows][32 m-cols]  (one per 32 columns of m)
 // Zero fill: every k (n) tail, the ψ rows [m, 8 mb) and the L columns
-// [m, 64) are zero-filled by the copies (so the padded T^T columns
+// [m, 32) of a half are zero-filled by the copies (so the padded T^T columns
 // are exactly zero); rows of R beyond the tile and of L beyond q only feed
 // accumulator rows / columns the epilogue never stores.
 #pragma once
@@ -63,28 +66,29 @@ struct FSeg {         // 48 B: one (ψ key, right op) product of a σ problem
   double scale;
 };
 
-constexpr int FKC = 64;             // n columns per STEP1 stage
-constexpr int FKLD = FKC + 2;       // K-contiguous row stride (≡ 2 mod 16: conflict-free LDS.64)
-constexpr int F_RT = 5;             // <= 5 column blocks per tile (40 σ columns)
+constexpr int FKC = 32;             // n columns per STEP1 stage
+constexpr int FKLD = FKC + 4;       // K-contiguous row stride (≡ 4 mod 16: the 16 lanes of an
+                                    // LDS.64 phase (rows lr, k lc) hit 16 distinct bank pairs)
+constexpr int F_RT = 4;             // <= 4 column blocks per tile (32 σ columns)
 constexpr int F_QB = 8;             // q <= 64
 constexpr int F_MB = 8;             // m <= 64
-constexpr int FLLD = 64 + 8;        // L stage row stride (≡ 8 mod 16: conflict-free LDS.128)
-constexpr int FCLD = 8 * F_RT + 10; // COPY row stride (≡ 2 mod 16)
+constexpr int FLLD = 32 + 8;        // L half row stride (≡ 8 mod 16: conflict-free LDS.128)
+constexpr int FCLD = 8 * F_RT + 2;  // COPY row stride (≡ 2 mod 16)
 constexpr int F_A_EL = 8 * F_RT * FKLD;
 constexpr int F_STAGE_EL = F_A_EL + 8 * F_MB * FKLD;
-static_assert(8 * F_QB * FLLD <= F_STAGE_EL, "L stage fits a stage");
+static_assert(8 * F_QB * FLLD <= F_STAGE_EL, "L half fits a stage");
 static_assert(8 * F_MB * FCLD <= F_STAGE_EL, "COPY stage fits a stage");
 #ifndef SDMRG_FMINB
-#define SDMRG_FMINB 1
+#define SDMRG_FMINB 2
 #endif
 #ifndef SDMRG_FSTAGES
 #define SDMRG_FSTAGES 3
 #endif
 constexpr int FSTAGES = SDMRG_FSTAGES;
-constexpr int F_SLD = 8 * F_QB + 2;                   // reduction scratch row stride
-constexpr int F_SCRATCH_EL = 8 * F_RT * F_SLD;
+constexpr int F_SLD = 8 * F_QB + 8;                   // reduction scratch row stride (≡ 8 mod 16)
+constexpr int F_SCRATCH_EL = 4 * 8 * F_SLD;           // one 8 x 64 σ^T slab per column block
 #ifndef SDMRG_FPRODUCERS
-#define SDMRG_FPRODUCERS 4
+#define SDMRG_FPRODUCERS 2
 #endif
 constexpr int F_PRODUCERS = SDMRG_FPRODUCERS;
 constexpr int F_THREADS = 32 * (4 + F_PRODUCERS);
@@ -92,10 +96,10 @@ constexpr int F_THREADS = 32 * (4 + F_PRODUCERS);
 struct FMeta {
   double* c;
   double scale;
-  int32_t type;      // 1 STEP1, 2 LSTAGE, 3 COPY
+  int32_t type;      // 1 STEP1, 2 LHALF, 3 COPY
   int32_t nks;       // STEP1: k4 steps in the stage
   int32_t mb;        // m blocks of the stage's product
-  int32_t half;      // unused
+  int32_t half;      // LHALF: which 32 columns of m
   int32_t flags;     // kFirst / kLast / kEnd / kSegEnd
   int32_t ldc, beta;
   int16_t q, rt;
@@ -109,6 +113,12 @@ __host__ __device__ constexpr int fused_smem_bytes() {
 
 __host__ __device__ inline int pad2d(int x) { return x + (x & 1); }
 
+// Column blocks per tile: 4, then 2 and 1 for the remainder (each tile keeps
+// all four DMMA warps busy: R = 2 / 1 split m between 2 / 4 warps).
+__host__ __device__ inline int fused_tile_blocks(int remaining_blocks) {
+  return remaining_blocks >= 4 ? 4 : (remaining_blocks >= 2 ? 2 : 1);
+}
+
 // The kernel itself is compiled in fused.cu only (runtime.h includes the
 // descriptor types above).
 #ifdef SDMRG_FUSED_KERNEL
@@ -117,111 +127,104 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 }
 
 // ------------------------------------------------------------------ consumer
-// One warp's part of one σ tile (RT column blocks, QB row blocks of σ):
-// stages until the tile's last, then the ordered 4-warp reduction.
-template <int RT, int QB>
-__device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_t& phase, int& g,
-                                           int w, int lane, double* scratch) {
+// One warp's part of one σ tile: column block a = w / S of the tile, m
+// blocks dealt S-ways; QB row blocks of σ.  Runs the tile's stages, then the
+// ordered S-way reduction and the (transposing) epilogue.
+template <int S, int QB>
+__device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_t& phase, int w,
+                                           int lane, double* scratch) {
+  constexpr int J = 8 / S;            // max m blocks this warp owns per product
   const int lr = lane >> 2, lc = lane & 3;
-  double sacc[RT][QB][2];
-  double tt[RT][2][2];
+  const int a = w / S, p = w % S;
+  double sacc[QB][2];
+  double tt[J][2];
 #pragma unroll
-  for (int a = 0; a < RT; ++a) {
+  for (int c = 0; c < QB; ++c) sacc[c][0] = sacc[c][1] = 0.0;
 #pragma unroll
-    for (int c = 0; c < QB; ++c) sacc[a][c][0] = sacc[a][c][1] = 0.0;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) tt[a][h][0] = tt[a][h][1] = 0.0;
-  }
+  for (int j = 0; j < J; ++j) tt[j][0] = tt[j][1] = 0.0;
   const FMeta& first = reinterpret_cast<const FMeta*>(ring.meta)[stage];
   double* const cbase = first.c;
   const int ldc = first.ldc, beta = first.beta, q = first.q, rt = first.rt;
-  g = 0;  // per-tile deal: the result depends on the tile only (bitwise determinism)
-  int j0 = (w - g) & 3;
+  int g = 0;  // m blocks dealt so far in this tile (per-tile: bitwise determinism)
   constexpr uint32_t STAGE_B = F_STAGE_EL * 8;
+  // owned block x (x < J) of a product: j = S x + ((p - g) mod S)
+  auto jof = [&](int x) { return S * x + ((p - g) & (S - 1)); };
   while (true) {
     const FMeta& m = reinterpret_cast<const FMeta*>(ring.meta)[stage];
     const int type = m.type, flags = m.flags, mb = m.mb;
     const uint32_t sa = ring.smem + stage * STAGE_B;
-    const bool v0 = j0 < mb, v1 = j0 + 4 < mb;
+    const int j0 = jof(0);
     if (type == 1) {
       // T^T[8a + lr][8j + ·] += R[8a + lr][k] ψ[8j + ·][k], k4 steps of 32 n
       const int nks = m.nks;
-      const uint32_t pa = sa + (lr * FKLD + lc) * 8;
+      const uint32_t pa = sa + ((8 * a + lr) * FKLD + lc) * 8;
       const uint32_t pb = sa + F_A_EL * 8 + ((8 * j0 + lr) * FKLD + lc) * 8;
-      auto body = [&](auto two_t) {
-        constexpr bool TWO = decltype(two_t)::value;
+      // owned blocks x < nj (warp-uniform): j0 + S x < mb
+      const int nj = j0 < mb ? (mb - j0 + S - 1) / S : 0;
+      auto body = [&](auto nj_t) {
+        constexpr int NJ = decltype(nj_t)::value;
 #pragma unroll
         for (int ks = 0; ks < FKC / 4; ++ks) {
           if (ks < nks) {
-            double af[RT];
+            const double af = lds64(pa + 4 * ks * 8);
+            double bf[NJ];
 #pragma unroll
-            for (int a = 0; a < RT; ++a) af[a] = lds64(pa + (8 * a * FKLD + 4 * ks) * 8);
-            const double b0 = lds64(pb + 4 * ks * 8);
-            double b1 = 0.0;
-            if (TWO) b1 = lds64(pb + (32 * FKLD + 4 * ks) * 8);
+            for (int x = 0; x < NJ; ++x) bf[x] = lds64(pb + (8 * S * x * FKLD + 4 * ks) * 8);
 #pragma unroll
-            for (int a = 0; a < RT; ++a) dmma(tt[a][0], af[a], b0);
-            if (TWO) {
-#pragma unroll
-              for (int a = 0; a < RT; ++a) dmma(tt[a][1], af[a], b1);
-            }
+            for (int x = 0; x < NJ; ++x) dmma(tt[x], af, bf[x]);
           }
         }
       };
-#ifndef FX_NOSTEP1
-      if (v1) body(std::true_type{});
-      else if (v0) body(std::false_type{});
-#endif
+      switch (nj) {
+        case 1: body(std::integral_constant<int, 1>{}); break;
+        case 2: if constexpr (J >= 2) body(std::integral_constant<int, 2>{}); break;
+        case 3: if constexpr (J >= 3) body(std::integral_constant<int, 3>{}); break;
+        case 4: if constexpr (J >= 4) body(std::integral_constant<int, 4>{}); break;
+        case 5: if constexpr (J >= 5) body(std::integral_constant<int, 5>{}); break;
+        case 6: if constexpr (J >= 6) body(std::integral_constant<int, 6>{}); break;
+        case 7: if constexpr (J >= 7) body(std::integral_constant<int, 7>{}); break;
+        case 8: if constexpr (J >= 8) body(std::integral_constant<int, 8>{}); break;
+        default: break;
+      }
     } else if (type == 3) {
       // identity R: T^T[8a + lr][8j + 2lc + e] = ψ[8j + 2lc + e][8a + lr]
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h == 0 ? v0 : v1) {
-          const uint32_t p = sa + ((8 * (j0 + 4 * h) + 2 * lc) * FCLD + lr) * 8;
-#pragma unroll
-          for (int a = 0; a < RT; ++a) {
-            tt[a][h][0] = lds64(p + 8 * a * 8);
-            tt[a][h][1] = lds64(p + (FCLD + 8 * a) * 8);
-          }
+      for (int x = 0; x < J; ++x) {
+        const int j = jof(x);
+        if (j < mb) {
+          const uint32_t pc = sa + ((8 * j + 2 * lc) * FCLD + 8 * a + lr) * 8;
+          tt[x][0] = lds64(pc);
+          tt[x][1] = lds64(pc + FCLD * 8);
         }
       }
     } else {
       // σ^T[8a + lr][8c + ·] += s T^T[8a + lr][8j + 2lc + e] L[8c + ·][8j + 2lc + e]
+      // for the owned blocks j inside this 32-column half of m
+      const int h = m.half;
       const double s = m.scale;
-      auto step2 = [&](auto h_t) {
-        constexpr int H = decltype(h_t)::value;
-        const uint32_t pl = sa + (lr * FLLD + 8 * (j0 + 4 * H) + 2 * lc) * 8;
-#ifndef FX_NOSCALE
-        if (__double_as_longlong(s) != 0x3FF0000000000000LL) {
+      const bool scaled = __double_as_longlong(s) != 0x3FF0000000000000LL;
 #pragma unroll
-          for (int a = 0; a < RT; ++a) {
-            tt[a][H][0] *= s;
-            tt[a][H][1] *= s;
+      for (int x = 0; x < J; ++x) {
+        const int j = jof(x);
+        if (j >= 4 * h && j < 4 * h + 4 && j < mb) {
+          if (scaled) {
+            tt[x][0] *= s;
+            tt[x][1] *= s;
+          }
+          const uint32_t pl = sa + (lr * FLLD + 8 * (j - 4 * h) + 2 * lc) * 8;
+#pragma unroll
+          for (int c = 0; c < QB; ++c) {
+            double b0, b1;
+            lds128(pl + 8 * c * FLLD * 8, b0, b1);
+            dmma(sacc[c], tt[x][0], b0);
+            dmma(sacc[c], tt[x][1], b1);
           }
         }
-#endif
-#pragma unroll
-        for (int c = 0; c < QB; ++c) {
-          double b0, b1;
-          lds128(pl + 8 * c * FLLD * 8, b0, b1);
-#pragma unroll
-          for (int a = 0; a < RT; ++a) {
-            dmma(sacc[a][c], tt[a][H][0], b0);
-            dmma(sacc[a][c], tt[a][H][1], b1);
-          }
-        }
-      };
-#ifndef FX_NOSTEP2
-      if (v0) step2(std::integral_constant<int, 0>{});
-      if (v1) step2(std::integral_constant<int, 1>{});
-#endif
+      }
       if (flags & kSegEnd) {
 #pragma unroll
-        for (int a = 0; a < RT; ++a)
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) tt[a][hh][0] = tt[a][hh][1] = 0.0;
+        for (int x = 0; x < J; ++x) tt[x][0] = tt[x][1] = 0.0;
         g += mb;
-        j0 = (w - g) & 3;
       }
     }
     __syncwarp();
@@ -233,67 +236,71 @@ __device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_
     if (flags & kLast) break;
     mbar_wait(ring.full0 + 8 * stage, phase);
   }
-  // ordered reduction of the four partial σ^T tiles: warp 0 stores, warps 1
-  // and 2 add, warp 3 adds and writes σ (transposed back); the last barrier
-  // frees the scratch for the next tile
-  const uint32_t sp = static_cast<uint32_t>(__cvta_generic_to_shared(scratch)) +
-                      (lr * F_SLD + 2 * lc) * 8;
+  // epilogue: the S warps of column block a sum their partial σ^T rows in
+  // order p = 0 .. S-1 through a scratch slab; the last writes σ (transposed)
+  const int col = 8 * a + lr;
+  auto store = [&]() {
+    if (col < rt) {
+#pragma unroll
+      for (int c = 0; c < QB; ++c) {
+        const int row = 8 * c + 2 * lc;
+        double* p0 = cbase + (int64_t)row * ldc + col;
+        if (row < q) *p0 = beta ? *p0 + sacc[c][0] : sacc[c][0];
+        if (row + 1 < q) p0[ldc] = beta ? p0[ldc] + sacc[c][1] : sacc[c][1];
+      }
+    }
+  };
+  if constexpr (S == 1) {
+    store();
+  } else {
+    const uint32_t sp = static_cast<uint32_t>(__cvta_generic_to_shared(scratch)) +
+                        ((a * 8 + lr) * F_SLD + 2 * lc) * 8;
 #pragma unroll 1
-  for (int s = 0; s < 4; ++s) {
-    if (w == s) {
+    for (int step = 0; step < S; ++step) {
+      if (p == step) {
+        if (step > 0) {
 #pragma unroll
-      for (int a = 0; a < RT; ++a)
-#pragma unroll
-        for (int c = 0; c < QB; ++c) {
-          const uint32_t p = sp + (8 * a * F_SLD + 8 * c) * 8;
-          double x = sacc[a][c][0], y = sacc[a][c][1];
-          if (s > 0) {
+          for (int c = 0; c < QB; ++c) {
             double u, v;
-            lds128(p, u, v);
-            x += u;
-            y += v;
-          }
-          if (s < 3) {
-            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(p), "d"(x), "d"(y) : "memory");
-          } else {
-            // σ[8c + 2lc + e][8a + lr] (tile-relative), rows < q, cols < rt
-            const int col = 8 * a + lr;
-            if (col < rt) {
-              const int row = 8 * c + 2 * lc;
-              double* p0 = cbase + (int64_t)row * ldc + col;
-              if (row < q) *p0 = beta ? *p0 + x : x;
-              if (row + 1 < q) p0[ldc] = beta ? p0[ldc] + y : y;
-            }
+            lds128(sp + 8 * c * 8, u, v);
+            sacc[c][0] += u;
+            sacc[c][1] += v;
           }
         }
+        if (step + 1 < S) {
+#pragma unroll
+          for (int c = 0; c < QB; ++c)
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(sp + 8 * c * 8),
+                         "d"(sacc[c][0]), "d"(sacc[c][1])
+                         : "memory");
+        } else {
+          store();
+        }
+      }
+      named_bar(1, 128);
     }
-    named_bar(1, 128);
   }
 }
 
-#define SDMRG_FCASE(RT, QB) \
-  case (RT) * 16 + (QB):    \
-    fused_tile<RT, QB>(ring, stage, phase, g, w, lane, scratch); \
+#define SDMRG_FCASE(S, QB) \
+  case (S) * 16 + (QB):    \
+    fused_tile<S, QB>(ring, stage, phase, w, lane, scratch); \
     break;
-#define SDMRG_FROW(RT)                                                                  \
-  SDMRG_FCASE(RT, 1) SDMRG_FCASE(RT, 2) SDMRG_FCASE(RT, 3) SDMRG_FCASE(RT, 4)           \
-  SDMRG_FCASE(RT, 5) SDMRG_FCASE(RT, 6) SDMRG_FCASE(RT, 7) SDMRG_FCASE(RT, 8)
+#define SDMRG_FROW(S)                                                                   \
+  SDMRG_FCASE(S, 1) SDMRG_FCASE(S, 2) SDMRG_FCASE(S, 3) SDMRG_FCASE(S, 4)               \
+  SDMRG_FCASE(S, 5) SDMRG_FCASE(S, 6) SDMRG_FCASE(S, 7) SDMRG_FCASE(S, 8)
 
 // ------------------------------------------------------------------ producer
-// F_PRODUCERS warps share every stage's copies (row r -> warp r mod
-// F_PRODUCERS): one warp issuing ~50 cp.async per lane and stage could not
-// keep four DMMA warps fed (ncu r2d: 14% DMMA-pipe activity with a single
-// producer, consumers spinning on the full barriers).
-//
-// 16-byte copies of `rows` rows x 64 K-columns of a row-major source (ld
-// even, column offset even), zero-filling columns >= kvalid and rows >=
-// rvalid; destination row stride LD.
+// F_PRODUCERS warps share every stage's copies (row r -> warp (r / 2) mod
+// F_PRODUCERS).  16-byte copies of `rows` rows x 32 K-columns of a
+// row-major source (ld even, column offset even), zero-filling columns >=
+// kvalid and rows >= rvalid; destination row stride LD.
 template <int LD>
-__device__ __forceinline__ void f_load_rows64(uint32_t sdst, const double* src, int ld, int rows,
+__device__ __forceinline__ void f_load_rows32(uint32_t sdst, const double* src, int ld, int rows,
                                               int rvalid, int kvalid, int lane, int pw) {
-  const int k = 2 * lane;
+  const int kp = lane & 15, k = 2 * kp;
   const int bytes = k + 1 < kvalid ? 16 : (k < kvalid ? 8 : 0);
-  for (int r = pw; r < rows; r += F_PRODUCERS) {
+  for (int r = (lane >> 4) + 2 * pw; r < rows; r += 2 * F_PRODUCERS) {
     const bool ok = r < rvalid && bytes > 0;
     cp_async16(sdst + (r * LD + k) * 8, ok ? src + (int64_t)r * ld + k : src, ok ? bytes : 0);
   }
@@ -367,8 +374,8 @@ __device__ __forceinline__ void fused_produce(const Ring& ring, const FTileRec* 
           const uint32_t st = ring.smem + stage * (F_STAGE_EL * 8);
           const int kv = n - c0;
           meta_write(1, (min(FKC, kv) + 3) >> 2, 0, 0);
-          f_load_rows64<FKLD>(st, rb + c0, pad2d(n), tr.rt, tr.rt, kv, lane, pw);
-          f_load_rows64<FKLD>(st + F_A_EL * 8, psi + c0, pad2d(n), 8 * mb, m, kv, lane, pw);
+          f_load_rows32<FKLD>(st, rb + c0, pad2d(n), tr.rt, tr.rt, kv, lane, pw);
+          f_load_rows32<FKLD>(st + F_A_EL * 8, psi + c0, pad2d(n), 8 * mb, m, kv, lane, pw);
           close();
         }
       } else {
@@ -388,11 +395,14 @@ __device__ __forceinline__ void fused_produce(const Ring& ring, const FTileRec* 
         close();
       }
       const double* l = res(sg.l);
-      open();
-      const uint32_t st = ring.smem + stage * (F_STAGE_EL * 8);
-      meta_write(2, 0, 0, kSegEnd | (last_seg ? kLast : 0));
-      f_load_rows64<FLLD>(st, l, pad2d(m), tr.q, tr.q, m, lane, pw);
-      close();
+      for (int h = 0; 32 * h < m; ++h) {
+        open();
+        const uint32_t st = ring.smem + stage * (F_STAGE_EL * 8);
+        const bool seg_end = 32 * (h + 1) >= m;
+        meta_write(2, 0, h, (seg_end ? kSegEnd : 0) | (seg_end && last_seg ? kLast : 0));
+        f_load_rows32<FLLD>(st, l + 32 * h, pad2d(m), tr.q, tr.q, m - 32 * h, lane, pw);
+        close();
+      }
     }
     t = next_tile();
   }
@@ -432,19 +442,16 @@ fused_heff_kernel(const FTileRec* __restrict__ tiles, int ntiles, const FSeg* __
     return;
   }
   const int w = warp;
-  int stage = 0, g = 0;
+  int stage = 0;
   uint32_t phase = 0;
   while (true) {
     mbar_wait(ring.full0 + 8 * stage, phase);
     const FMeta& m = meta[stage];
     if (m.flags & kEnd) break;
     const int rtb = (m.rt + 7) >> 3, qb = (m.q + 7) >> 3;
-    switch (rtb * 16 + qb) {
-#ifdef SDMRG_FONE
-      SDMRG_FCASE(5, 8)
-#else
-      SDMRG_FROW(1) SDMRG_FROW(2) SDMRG_FROW(3) SDMRG_FROW(4) SDMRG_FROW(5)
-#endif
+    const int sw = 4 / fused_tile_blocks(rtb);   // m-split factor S
+    switch (sw * 16 + qb) {
+      SDMRG_FROW(1) SDMRG_FROW(2) SDMRG_FROW(4)
       default: __trap();
     }
   }

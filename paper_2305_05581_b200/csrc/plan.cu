@@ -182,6 +182,7 @@ struct sdmrg_plan {
   cudaEvent_t fork = nullptr, join = nullptr;
   sdmrg_plan_stats stats{};
   int64_t fused_outs = 0;          // σ problems on the fused kernel
+  double shard_balance = 1.0;      // mean / max rank load (world > 1)
   int timing = 0;
 };
 
@@ -402,9 +403,6 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
 
   const std::vector<int32_t> shL = shift_table(d->nops_l, d->delta_l, nL, d->qn_l, nc);
   const std::vector<int32_t> shR = shift_table(d->nops_r, d->delta_r, nR, d->qn_r, nc);
-  std::vector<int64_t> poff_l, poff_r;
-  const int64_t psize_l = pad_offsets(d->nops_l, nL, d->blk_off_l, shL.data(), d->dim_l, false, poff_l);
-  const int64_t psize_r = pad_offsets(d->nops_r, nR, d->blk_off_r, shR.data(), d->dim_r, true, poff_r);
   plan->stack_t = !plan->tiled && getenv("SDMRG_NO_STACK_T") == nullptr;
 
   // ---- task generation: members per ψ key, rows in table order
@@ -524,24 +522,84 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     }
   }
 
-  // ---- shard ψ keys over ranks (greedy LPT on phase-2 cost, deterministic)
+  // ---- shard ψ keys over ranks (greedy LPT on executed cost, deterministic).
+  // Default: whole left column sectors (every ψ key with the same left
+  // sector) go to one rank, so a rank reads — and holds — only the left
+  // operator blocks of its own sectors and the right blocks they pair with:
+  // operator memory scales with the rank count.  SDMRG_SHARD=key deals single
+  // ψ keys instead (finest balance, every rank touches nearly every block).
   std::vector<char> mine(nk, 1);
   if (d->world > 1) {
-    std::vector<int64_t> order(nk);
+    const char* sm = getenv("SDMRG_SHARD");
+    const bool by_key = sm && std::strcmp(sm, "key") == 0;
+    // units: whole left sectors, except a sector heavier than half a rank's
+    // share, whose ψ keys are dealt singly (one central sector can exceed
+    // 1/8 of the work at L=30 D=2048)
+    std::vector<double> jcost(nL, 0.0);
+    double tot = 0.0;
+    for (int64_t i = 0; i < nk; ++i) {
+      jcost[keys[i].jl] += key_cost[i] + 1.0;
+      tot += key_cost[i] + 1.0;
+    }
+    std::vector<int64_t> unit_of(nk);
+    std::vector<double> ucost;
+    std::vector<int64_t> jl_unit(nL, -1);
+    for (int64_t i = 0; i < nk; ++i) {
+      const int jl = keys[i].jl;
+      if (by_key || jcost[jl] > tot / (2.0 * d->world)) {
+        unit_of[i] = static_cast<int64_t>(ucost.size());
+        ucost.push_back(key_cost[i] + 1.0);
+      } else {
+        if (jl_unit[jl] < 0) {
+          jl_unit[jl] = static_cast<int64_t>(ucost.size());
+          ucost.push_back(0.0);
+        }
+        unit_of[i] = jl_unit[jl];
+        ucost[jl_unit[jl]] += key_cost[i] + 1.0;
+      }
+    }
+    const int64_t nunit = static_cast<int64_t>(ucost.size());
+    std::vector<int64_t> order(nunit);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(),
-                     [&](int64_t a, int64_t b) { return key_cost[a] > key_cost[b]; });
+                     [&](int64_t a, int64_t b) { return ucost[a] > ucost[b]; });
     std::vector<double> load(d->world, 0.0);
-    for (int64_t idx : order) {
+    std::vector<int> owner(nunit, 0);
+    for (int64_t u : order) {
       int best = 0;
       for (int w = 1; w < d->world; ++w)
         if (load[w] < load[best]) best = w;
-      load[best] += key_cost[idx] + 1.0;
-      mine[idx] = (best == d->rank);
+      load[best] += ucost[u];
+      owner[u] = best;
     }
+    for (int64_t i = 0; i < nk; ++i) mine[i] = owner[unit_of[i]] == d->rank;
+    double mx = 0.0;
+    for (double x : load) mx = std::max(mx, x);
+    plan->shard_balance = mx > 0.0 ? tot / (d->world * mx) : 1.0;
   }
 
   plan->mine = mine;
+
+  // ---- padded arenas: the blocks this rank's ψ keys read (all of them at
+  // world 1), column-sector-major
+  std::vector<int64_t> poff_l, poff_r;
+  int64_t psize_l, psize_r;
+  {
+    std::vector<int64_t> use_l((size_t)d->nops_l * nL, -1), use_r((size_t)d->nops_r * nR, -1);
+    for (int64_t i = 0; i < nk; ++i) {
+      if (!mine[i]) continue;
+      for (const Pair& p : pairs[i]) {
+        const size_t xr = (size_t)p.rop * nR + keys[i].jr;
+        use_r[xr] = d->blk_off_r[xr];
+        for (int32_t t = p.term_begin; t < p.term_end; ++t) {
+          const size_t xl = (size_t)terms[i][t].lop * nL + keys[i].jl;
+          use_l[xl] = d->blk_off_l[xl];
+        }
+      }
+    }
+    psize_l = pad_offsets(d->nops_l, nL, use_l.data(), shL.data(), d->dim_l, false, poff_l);
+    psize_r = pad_offsets(d->nops_r, nR, use_r.data(), shR.data(), d->dim_r, true, poff_r);
+  }
 
   // ---- fused small-sector σ problems (fused.cuh): an out key whose rows q
   // and every contributing ψ key's rows m are <= 64 is evaluated by the fused
@@ -905,8 +963,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       const size_t nseg = fz ? op.fsegs.size() : op.segs.size();
       double tile_cost;
       if (fz) {
-        const int rb = (op.r + 7) / 8, nt = (rb + F_RT - 1) / F_RT;
-        tile_cost = op.fcost / nt;
+        const int rb = (op.r + 7) / 8;
+        tile_cost = op.fcost * std::min(rb, F_RT) / rb;  // the widest column tile's share
       } else {
         tile_cost = double(op.q) / tiles_of(op.q) * (double(op.r) / tiles_of(op.r)) * op.ksum;
       }
@@ -974,6 +1032,10 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   int64_t ws_max = 0;
   for (auto& ch : plan->chunks) ws_max = std::max(ws_max, ch.ws_doubles);
   rc = SDMRG_OK;
+  plan->arena_size[0] = psize_l;
+  plan->arena_size[1] = psize_r;
+  plan->arena_off[0] = poff_l;
+  plan->arena_off[1] = poff_r;
   if (!d->dry_run) {
     // padded device copies of the arenas and ψ; zeroed so every pad is 0
     auto repack = [&](const double* src, const int64_t* boff, const std::vector<int64_t>& poff,
@@ -1006,10 +1068,6 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       pl.release();
       return r;
     };
-    plan->arena_size[0] = psize_l;
-    plan->arena_size[1] = psize_r;
-    plan->arena_off[0] = poff_l;
-    plan->arena_off[1] = poff_r;
     rc = repack(d->arena_l, d->blk_off_l, poff_l, shL, d->dim_l, d->nops_l, nL, psize_l,
                 &plan->arena_l);
     if (!rc)
@@ -1108,6 +1166,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   st.combine_terms = comb_terms;
   st.fused_outs = plan->fused_outs;
   st.arena_bytes = 8 * (psize_l + psize_r);
+  st.shard_balance_ppm = static_cast<int64_t>(plan->shard_balance * 1e6);
   *out = plan;
   return SDMRG_OK;
 }

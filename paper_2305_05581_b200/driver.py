@@ -19,6 +19,7 @@ The ``Engine`` hooks (plan factory, Lanczos, grouped-GEMM runner) default to
 the sm_100a library; tests may substitute checkers, the product never does.
 """
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -686,6 +687,8 @@ class StoreDict(dict):
     def __init__(self, device=None, budget=None):
         super().__init__()
         self.device = device
+        if budget is None and os.environ.get("SDMRG_STORE_BUDGET"):
+            budget = int(float(os.environ["SDMRG_STORE_BUDGET"]))
         if budget is None and device is not None and device.type == "cuda":
             budget = int(0.35 * torch.cuda.get_device_properties(device).total_memory)
         self.budget = budget

@@ -202,6 +202,18 @@ class DevicePlan:
         view = torch.as_tensor(_View(), device=self.device)
         return view, offs
 
+    def block_layout(self, side):
+        """offsets[nops, nsec] of the operator blocks this plan holds in its
+        padded arena for side 'l' / 'r' (-1: not held — blocks no ψ sector of
+        this rank reads); available in dry runs too."""
+        k = {"l": 0, "r": 1}[side]
+        nops = self.pi.kind_l.shape[0] if k == 0 else self.pi.kind_r.shape[0]
+        nsec = self.pi.dim_l.shape[0] if k == 0 else self.pi.dim_r.shape[0]
+        offs = np.zeros((nops, nsec), np.int64)
+        _lib.check(_lib.load().sdmrg_plan_arena(self._h, k, None, None,
+                                                _lib.as_p(offs, ctypes.c_int64)))
+        return offs
+
     def shard(self):
         """Boolean mask over ψ keys: the input sectors this rank applies."""
         mine = np.zeros(self.stats["psi_keys"], np.int32)

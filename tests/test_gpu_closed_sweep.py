@@ -119,3 +119,19 @@ def test_closed_loop_configs0_L16_D256():
     st = _run(hdr["L"], hdr["model_seed"], hdr["run_seed"], hdr["D"], hdr["sweeps"],
               hdr["lanczos_tol"], hdr["lanczos_max_iter"])
     _compare(st, ref, check_iters=False, min_compared=0)
+
+
+def test_store_offload_is_transparent(monkeypatch):
+    """Block stores beyond the HBM budget wait in host memory (driver.StoreDict):
+    with a budget of one byte every store not in use is offloaded and fetched
+    back, and the run matches the all-resident one."""
+    hdr, _ = _load_record("sweep_record_L8_D32.jsonl")
+    base = _run(hdr["L"], hdr["model_seed"], hdr["run_seed"], hdr["D"], 1,
+                hdr["lanczos_tol"], hdr["lanczos_max_iter"])
+    monkeypatch.setenv("SDMRG_STORE_BUDGET", "1")
+    off = _run(hdr["L"], hdr["model_seed"], hdr["run_seed"], hdr["D"], 1,
+               hdr["lanczos_tol"], hdr["lanczos_max_iter"])
+    assert off.left.offloads + off.right.offloads > 0
+    assert len(off.records) == len(base.records)
+    for a, b in zip(off.records, base.records):
+        assert abs(a.energy - b.energy) <= 1e-12

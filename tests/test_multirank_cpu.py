@@ -37,6 +37,15 @@ def _worker(rank, world, port, case, outq):
     pi = PlanInput.load(os.path.join(GOLDEN, case + ".npz"))
     plan = DevicePlan(pi, rank=rank, world=world, dry_run=True)
     mine = plan.shard()
+    # the rank holds only the operator blocks its ψ sectors read: zero every
+    # other block — the shard's partial σ must not change
+    for side, arena, boff in (("l", pi.arena_l, pi.blk_off_l), ("r", pi.arena_r, pi.blk_off_r)):
+        held = plan.block_layout(side) >= 0
+        dim = pi.dim_l if side == "l" else pi.dim_r
+        from paper_2305_05581_b200.workload import _rows_of
+        for o, j in zip(*np.nonzero((boff >= 0) & ~held)):
+            n = _rows_of(pi, side, o, j) * int(dim[j])
+            arena[boff[o, j]:boff[o, j] + n] = 0.0
     groups = [g for g in heff.build_groups(pi) if mine[g[0]]]
     part = heff.apply_groups(pi, groups, pi.meta["psi"])
     t = torch.from_numpy(part)
@@ -44,7 +53,9 @@ def _worker(rank, world, port, case, outq):
     owned = torch.from_numpy(mine.astype(np.int64))
     dist.all_reduce(owned)
     outq.put((rank, t.numpy().copy(), owned.numpy().copy(),
-              int(plan.stats["local_members"]), int(plan.stats["members"])))
+              int(plan.stats["local_members"]), int(plan.stats["members"]),
+              int(plan.stats["arena_bytes"]),
+              int(DevicePlan(pi, dry_run=True).stats["arena_bytes"])))
     dist.destroy_process_group()
 
 
@@ -66,8 +77,10 @@ def test_gloo_world2_sharded_sigma_allreduce(case):
     ref = pi.meta["sigma"]
     scale = 1.0 + np.max(np.abs(ref))
     local = 0
-    for _rank, sigma, owned, lm, total in res:
+    for _rank, sigma, owned, lm, total, held, full in res:
         assert np.max(np.abs(sigma - ref)) <= 1e-12 * scale
         assert np.all(owned == 1)            # every ψ key owned by exactly one rank
+        assert held <= full                  # per-rank operator arenas never exceed world 1
         local += lm
+    assert sum(r[5] for r in res) < 2 * res[0][6] or res[0][6] == 0
     assert local == res[0][4]                # members partitioned

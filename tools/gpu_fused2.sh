@@ -5,7 +5,7 @@ OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $OUT/gpu.txt 2>&1
 timeout 600 python -m pytest tests/test_gpu_parity.py -q > $OUT/pytest_parity.log 2>&1; echo "rc=$?" >> $OUT/pytest_parity.log
-for cfg in "76 4096 113" "50 4096" "30 1024"; do
+for cfg in "76 4096 113" "50 4096"; do
   for f in 1 0; do
     echo "[fused=$f] $cfg: $(SDMRG_FUSED=$f timeout 600 python tools/quick.py $cfg 2>&1 | tail -1)" >> $OUT/quick.log
   done
