@@ -239,6 +239,13 @@ int sdmrg_gemv_t(int k, int64_t n, const double* v, int64_t ldv,
 int sdmrg_gemv_n(int k, int64_t n, const double* v, int64_t ldv,
                  const double* coef_dev, double sign, double* w, void* stream);
 /* x *= s where s = num/den read from device scalars (den NULL -> 1).        */
+/* One classical Gram-Schmidt pass of the device Lanczos (dmrg.py:67-71
+ * reorthogonalisation) over a Krylov basis held as nslabs (<= 16) slabs of
+ * slab_rows contiguous length-n vectors (k vectors in all):
+ *   coef = V^T w;  w -= V coef;  and, if norm_dev, *norm_dev = ||w|| after.
+ * Four launches whatever k is; fixed-order reductions (bitwise repeatable). */
+int sdmrg_krylov_project(int nslabs, const double* const* slabs, int slab_rows, int k, int64_t n,
+                         double* w, double* coef_dev, double* norm_dev, void* stream);
 int sdmrg_scal_dev(int64_t n, const double* num_dev, const double* den_dev,
                    int invert_den, double* x, void* stream);
 /* y = a*x + b*y with host scalars.                                          */

@@ -92,6 +92,7 @@ _SIGS = {
     "sdmrg_nrm2": (c_int, [c_i64, c_vp, c_vp, c_vp]),
     "sdmrg_gemv_t": (c_int, [c_int, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "sdmrg_gemv_n": (c_int, [c_int, c_i64, c_vp, c_i64, c_vp, c_dbl, c_vp, c_vp]),
+    "sdmrg_krylov_project": (c_int, [c_int, c_vp, c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "sdmrg_scal_dev": (c_int, [c_i64, c_vp, c_vp, c_int, c_vp, c_vp]),
     "sdmrg_axpby": (c_int, [c_i64, c_dbl, c_vp, c_dbl, c_vp, c_vp]),
     "sdmrg_rotate": (c_int, [c_i64, P_i64, P_i64, P_i64, P_i64, P_i32, P_i32, P_i32, P_i32,

@@ -394,7 +394,7 @@ def _head_products(out, keys, ops, marena, mkeys):
         cl_m, r_m = marena.ops[mk]
         cl_h, r_h = ops.ops[h]
         j = cl_o.col
-        if len(j) == 0:
+        if len(j) == 0 or len(cl_m.row) == 0 or len(cl_h.row) == 0:
             continue
         ms = _slot_table(cl_m, nsec)[j]
         ok = ms >= 0

@@ -180,7 +180,7 @@ constexpr int THREADS = 32 * (CONSUMERS + PRODUCERS);
 // step) then hits 16 distinct bank pairs per half-warp; the padded stride 18
 // maps rows lr and lr + 1 two bank pairs apart (2-way conflicts for lc >= 2).
 #ifndef SDMRG_SWZ
-#define SDMRG_SWZ 0
+#define SDMRG_SWZ 1
 #endif
 constexpr int KC_LD = SDMRG_SWZ ? BK : BK + 2;   // K-contiguous row stride
 constexpr int NC_LD_A = BM + 4;                  // M-contiguous A row stride

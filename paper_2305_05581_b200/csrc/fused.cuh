@@ -130,9 +130,14 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 // One warp's part of one σ tile: column block a = w / S of the tile, m
 // blocks dealt S-ways; QB row blocks of σ.  Runs the tile's stages, then the
 // ordered S-way reduction and the (transposing) epilogue.
-template <int S, int QB>
+template <int S>
 __device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_t& phase, int w,
                                            int lane, double* scratch) {
+  // one body per m-split S (three in all): the σ row-block count qb and the
+  // owned m-block count are warp-uniform runtime guards around unrolled
+  // loops, not template parameters — 24 shape bodies (r2g) spent 30% of the
+  // stall samples on instruction-cache misses
+  constexpr int QB = F_QB;
   constexpr int J = 8 / S;            // max m blocks this warp owns per product
   const int lr = lane >> 2, lc = lane & 3;
   const int a = w / S, p = w % S;
@@ -145,54 +150,34 @@ __device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_
   const FMeta& first = reinterpret_cast<const FMeta*>(ring.meta)[stage];
   double* const cbase = first.c;
   const int ldc = first.ldc, beta = first.beta, q = first.q, rt = first.rt;
+  const int qb = (q + 7) >> 3;
   int g = 0;  // m blocks dealt so far in this tile (per-tile: bitwise determinism)
   constexpr uint32_t STAGE_B = F_STAGE_EL * 8;
-  // owned block x (x < J) of a product: j = S x + ((p - g) mod S)
-  auto jof = [&](int x) { return S * x + ((p - g) & (S - 1)); };
   while (true) {
     const FMeta& m = reinterpret_cast<const FMeta*>(ring.meta)[stage];
     const int type = m.type, flags = m.flags, mb = m.mb;
     const uint32_t sa = ring.smem + stage * STAGE_B;
-    const int j0 = jof(0);
+    // owned blocks of this product: j = j0 + S x, x < nj
+    const int j0 = (p - g) & (S - 1);
+    const int nj = j0 < mb ? (mb - j0 + S - 1) / S : 0;
     if (type == 1) {
       // T^T[8a + lr][8j + ·] += R[8a + lr][k] ψ[8j + ·][k], k4 steps of 32 n
       const int nks = m.nks;
       const uint32_t pa = sa + ((8 * a + lr) * FKLD + lc) * 8;
       const uint32_t pb = sa + F_A_EL * 8 + ((8 * j0 + lr) * FKLD + lc) * 8;
-      // owned blocks x < nj (warp-uniform): j0 + S x < mb
-      const int nj = j0 < mb ? (mb - j0 + S - 1) / S : 0;
-      auto body = [&](auto nj_t) {
-        constexpr int NJ = decltype(nj_t)::value;
+#pragma unroll 2
+      for (int ks = 0; ks < nks; ++ks) {
+        const double af = lds64(pa + 4 * ks * 8);
 #pragma unroll
-        for (int ks = 0; ks < FKC / 4; ++ks) {
-          if (ks < nks) {
-            const double af = lds64(pa + 4 * ks * 8);
-            double bf[NJ];
-#pragma unroll
-            for (int x = 0; x < NJ; ++x) bf[x] = lds64(pb + (8 * S * x * FKLD + 4 * ks) * 8);
-#pragma unroll
-            for (int x = 0; x < NJ; ++x) dmma(tt[x], af, bf[x]);
-          }
-        }
-      };
-      switch (nj) {
-        case 1: body(std::integral_constant<int, 1>{}); break;
-        case 2: if constexpr (J >= 2) body(std::integral_constant<int, 2>{}); break;
-        case 3: if constexpr (J >= 3) body(std::integral_constant<int, 3>{}); break;
-        case 4: if constexpr (J >= 4) body(std::integral_constant<int, 4>{}); break;
-        case 5: if constexpr (J >= 5) body(std::integral_constant<int, 5>{}); break;
-        case 6: if constexpr (J >= 6) body(std::integral_constant<int, 6>{}); break;
-        case 7: if constexpr (J >= 7) body(std::integral_constant<int, 7>{}); break;
-        case 8: if constexpr (J >= 8) body(std::integral_constant<int, 8>{}); break;
-        default: break;
+        for (int x = 0; x < J; ++x)
+          if (x < nj) dmma(tt[x], af, lds64(pb + (8 * S * x * FKLD + 4 * ks) * 8));
       }
     } else if (type == 3) {
       // identity R: T^T[8a + lr][8j + 2lc + e] = ψ[8j + 2lc + e][8a + lr]
 #pragma unroll
       for (int x = 0; x < J; ++x) {
-        const int j = jof(x);
-        if (j < mb) {
-          const uint32_t pc = sa + ((8 * j + 2 * lc) * FCLD + 8 * a + lr) * 8;
+        if (x < nj) {
+          const uint32_t pc = sa + ((8 * (j0 + S * x) + 2 * lc) * FCLD + 8 * a + lr) * 8;
           tt[x][0] = lds64(pc);
           tt[x][1] = lds64(pc + FCLD * 8);
         }
@@ -205,8 +190,8 @@ __device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_
       const bool scaled = __double_as_longlong(s) != 0x3FF0000000000000LL;
 #pragma unroll
       for (int x = 0; x < J; ++x) {
-        const int j = jof(x);
-        if (j >= 4 * h && j < 4 * h + 4 && j < mb) {
+        const int j = j0 + S * x;
+        if (x < nj && j >= 4 * h && j < 4 * h + 4) {
           if (scaled) {
             tt[x][0] *= s;
             tt[x][1] *= s;
@@ -214,10 +199,12 @@ __device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_
           const uint32_t pl = sa + (lr * FLLD + 8 * (j - 4 * h) + 2 * lc) * 8;
 #pragma unroll
           for (int c = 0; c < QB; ++c) {
-            double b0, b1;
-            lds128(pl + 8 * c * FLLD * 8, b0, b1);
-            dmma(sacc[c], tt[x][0], b0);
-            dmma(sacc[c], tt[x][1], b1);
+            if (c < qb) {
+              double b0, b1;
+              lds128(pl + 8 * c * FLLD * 8, b0, b1);
+              dmma(sacc[c], tt[x][0], b0);
+              dmma(sacc[c], tt[x][1], b1);
+            }
           }
         }
       }
@@ -281,14 +268,6 @@ __device__ __forceinline__ void fused_tile(const Ring& ring, int& stage, uint32_
     }
   }
 }
-
-#define SDMRG_FCASE(S, QB) \
-  case (S) * 16 + (QB):    \
-    fused_tile<S, QB>(ring, stage, phase, w, lane, scratch); \
-    break;
-#define SDMRG_FROW(S)                                                                   \
-  SDMRG_FCASE(S, 1) SDMRG_FCASE(S, 2) SDMRG_FCASE(S, 3) SDMRG_FCASE(S, 4)               \
-  SDMRG_FCASE(S, 5) SDMRG_FCASE(S, 6) SDMRG_FCASE(S, 7) SDMRG_FCASE(S, 8)
 
 // ------------------------------------------------------------------ producer
 // F_PRODUCERS warps share every stage's copies (row r -> warp (r / 2) mod
@@ -448,16 +427,14 @@ fused_heff_kernel(const FTileRec* __restrict__ tiles, int ntiles, const FSeg* __
     mbar_wait(ring.full0 + 8 * stage, phase);
     const FMeta& m = meta[stage];
     if (m.flags & kEnd) break;
-    const int rtb = (m.rt + 7) >> 3, qb = (m.q + 7) >> 3;
-    const int sw = 4 / fused_tile_blocks(rtb);   // m-split factor S
-    switch (sw * 16 + qb) {
-      SDMRG_FROW(1) SDMRG_FROW(2) SDMRG_FROW(4)
-      default: __trap();
+    const int rtb = (m.rt + 7) >> 3;
+    switch (4 / fused_tile_blocks(rtb)) {   // m-split factor S
+      case 1: fused_tile<1>(ring, stage, phase, w, lane, scratch); break;
+      case 2: fused_tile<2>(ring, stage, phase, w, lane, scratch); break;
+      default: fused_tile<4>(ring, stage, phase, w, lane, scratch); break;
     }
   }
 }
-#undef SDMRG_FCASE
-#undef SDMRG_FROW
 #endif  // SDMRG_FUSED_KERNEL
 
 }  // namespace sdmrg

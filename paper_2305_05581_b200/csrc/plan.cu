@@ -604,11 +604,13 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   // ---- fused small-sector σ problems (fused.cuh): an out key whose rows q
   // and every contributing ψ key's rows m are <= 64 is evaluated by the fused
   // kernel (T = ψ R^T chained in registers, never stored); the others by the
-  // two-phase engine.  SDMRG_FUSED=0 turns the fused path off.
+  // two-phase engine.  SDMRG_FUSED=1 turns the fused path on.
   std::vector<char> fuse_out(nk, 0);
   {
+    // off by default: on one B200 the fused kernel is still slower than the
+    // two-phase engine (L=76 D=4096: 393-400 vs 238-249 ms, profiles/r2_notes.md)
     const char* fe = getenv("SDMRG_FUSED");
-    const bool allow = !(fe && fe[0] == '0');
+    const bool allow = fe && fe[0] == '1';
     if (allow) {
       std::vector<int> maxm(nk, 0);
       for (int64_t i = 0; i < nk; ++i) {

@@ -89,6 +89,69 @@ __global__ void axpby_kernel(int64_t n, double a, const double* __restrict__ x, 
     y[i] = (b == 0.0) ? a * x[i] : a * x[i] + b * y[i];  // b == 0: y may be garbage
 }
 
+// Krylov basis as up to kMaxSlabs slabs of slab_rows contiguous vectors
+// (lanczos.py KrylovBasis): one launch per reduction / update over all of
+// them instead of one per slab.
+constexpr int kMaxSlabs = 16;
+struct SlabTable {
+  const double* p[kMaxSlabs];
+};
+
+__global__ void dots_partial_slabs(int64_t n, SlabTable t, int slab_rows,
+                                   const double* __restrict__ w, double* __restrict__ partial) {
+  const int row = blockIdx.y;
+  const double* vr = t.p[row / slab_rows] + (int64_t)(row % slab_rows) * n;
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = min(n, lo + chunk);
+  double s = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += vr[i] * w[i];
+  s = warp_sum(s);
+  __shared__ double red[kRedThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double u = threadIdx.x < kRedThreads / 32 ? red[threadIdx.x] : 0.0;
+    u = warp_sum(u);
+    if (threadIdx.x == 0) partial[(int64_t)row * gridDim.x + blockIdx.x] = u;
+  }
+}
+
+// w[j] -= sum_i coef[i] V_i[j] over all slabs; optionally the per-block
+// partial sums of the updated w[j]^2 (the norm of the projected vector,
+// fused into the same pass over w)
+__global__ void gemv_n_slabs(int k, int64_t n, SlabTable t, int slab_rows,
+                             const double* __restrict__ coef, double* __restrict__ w,
+                             double* __restrict__ sq_partial) {
+  extern __shared__ double sc[];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) sc[i] = coef[i];
+  __syncthreads();
+  double sq = 0.0;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int sl = 0, i0 = 0; i0 < k; ++sl, i0 += slab_rows) {
+      const double* v = t.p[sl] + j;
+      const int ie = min(k - i0, slab_rows);
+      for (int i = 0; i < ie; ++i) s += sc[i0 + i] * v[(int64_t)i * n];
+    }
+    const double x = w[j] - s;
+    w[j] = x;
+    sq += x * x;
+  }
+  if (sq_partial) {
+    sq = warp_sum(sq);
+    __shared__ double red[kRedThreads / 32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double u = threadIdx.x < kRedThreads / 32 ? red[threadIdx.x] : 0.0;
+      u = warp_sum(u);
+      if (threadIdx.x == 0) sq_partial[blockIdx.x] = u;
+    }
+  }
+}
+
 static int grid_for_n(int64_t n) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
 }
@@ -162,6 +225,37 @@ int sdmrg_gemv_n(int k, int64_t n, const double* v, int64_t ldv, const double* c
       k, n, v, ldv, coef_dev, sign, w);
   count_launch();
   return cuda_check(cudaGetLastError(), "gemv_n launch");
+}
+
+int sdmrg_krylov_project(int nslabs, const double* const* slabs, int slab_rows, int k, int64_t n,
+                         double* w, double* coef_dev, double* norm_dev, void* stream_) {
+  if (k < 0 || n < 0 || slab_rows <= 0 || nslabs < 0 || nslabs > kMaxSlabs ||
+      (int64_t)nslabs * slab_rows < k || (k > 0 && !slabs))
+    return fail(SDMRG_EINVAL, "krylov_project: bad arguments");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  SlabTable t{};
+  for (int i = 0; i < nslabs; ++i) t.p[i] = slabs[i];
+  const int gn = grid_for_n(n);
+  double* partial = nullptr;
+  int rc = partials_for(stream, (size_t)std::max(k, 1) * kRedBlocks + gn, &partial);
+  if (rc) return rc;
+  double* sq = partial + (size_t)std::max(k, 1) * kRedBlocks;
+  if (k > 0) {
+    dots_partial_slabs<<<dim3(kRedBlocks, k), kRedThreads, 0, stream>>>(n, t, slab_rows, w, partial);
+    dots_final<<<(k + 7) / 8, 256, 0, stream>>>(k, kRedBlocks, partial, coef_dev, 0);
+    count_launch(2);
+  }
+  if (n > 0 && (k > 0 || norm_dev)) {
+    gemv_n_slabs<<<gn, kRedThreads, sizeof(double) * std::max(k, 1), stream>>>(
+        k, n, t, slab_rows, coef_dev, w, norm_dev ? sq : nullptr);
+    count_launch();
+  }
+  if (norm_dev) {
+    if (n == 0) return cuda_check(cudaMemsetAsync(norm_dev, 0, sizeof(double), stream), "norm");
+    dots_final<<<1, 32, 0, stream>>>(1, gn, sq, norm_dev, 1);
+    count_launch();
+  }
+  return cuda_check(cudaGetLastError(), "krylov_project launch");
 }
 
 int sdmrg_scal_dev(int64_t n, const double* num_dev, const double* den_dev, int invert_den,

@@ -10,15 +10,18 @@ tridiagonal Ritz problem the reference also solves on the host
 Reorthogonalisation: the reference subtracts alpha v_k and beta v_{k-1} and
 then runs one modified Gram-Schmidt sweep over the basis (dmrg.py:67-71).
 Here the same projector is applied as two classical Gram-Schmidt passes
-(CGS2: coef = V^T w; w -= V coef; twice), each pass two bandwidth-bound
-kernels over the stored basis; alpha is the first pass's coefficient on v_k
-(before any subtraction, exactly the reference's alpha).
+(CGS2: coef = V^T w; w -= V coef; twice), each pass one fixed set of
+launches over all basis slabs (sdmrg_krylov_project: dot partials, their
+fixed-order sum, the update — the second pass also yields ||w||); alpha is
+the first pass's coefficient on v_k (before any subtraction, exactly the
+reference's alpha).
 """
 
 from typing import NamedTuple
 
 import numpy as np
 import torch
+from scipy.linalg import eigh_tridiagonal
 
 from . import _lib
 
@@ -60,12 +63,21 @@ class KrylovBasis:
         self.count += 1
         return v
 
-    def project_out(self, w, stream, coef_out=None):
-        """One CGS pass: coef = V^T w ; w -= V coef.  Returns coef (device)."""
+    def project_out(self, w, stream, coef_out=None, norm_out=None):
+        """One CGS pass: coef = V^T w ; w -= V coef (sdmrg_krylov_project:
+        one launch set over all slabs; ``norm_out`` receives ||w|| after the
+        update).  Returns coef (device)."""
         lib = _lib.load()
         if self.count > self.coef.numel():
             self.coef = torch.zeros(2 * self.count, dtype=torch.float64, device=self.device)
         coef = self.coef if coef_out is None else coef_out
+        nsl = (self.count + _CHUNK - 1) // _CHUNK
+        if nsl <= 16:
+            ptrs = (_lib.c_vp * max(nsl, 1))(*[s.data_ptr() for s in self.slabs[:nsl]])
+            _lib.check(lib.sdmrg_krylov_project(
+                nsl, ptrs, _CHUNK, self.count, self.n, w.data_ptr(), coef.data_ptr(),
+                None if norm_out is None else norm_out.data_ptr(), stream))
+            return coef
         for s, slab in enumerate(self.slabs):
             k = min(_CHUNK, self.count - s * _CHUNK)
             if k <= 0:
@@ -80,6 +92,8 @@ class KrylovBasis:
             c = coef[s * _CHUNK:s * _CHUNK + k]
             _lib.check(lib.sdmrg_gemv_n(k, self.n, slab.data_ptr(), self.n, c.data_ptr(),
                                         -1.0, w.data_ptr(), stream))
+        if norm_out is not None:
+            _nrm2(w, norm_out, stream)
         return coef
 
     def combine(self, coefs, out, stream):
@@ -103,6 +117,14 @@ def _nrm2(x, out, stream):
 def _axpby(a, x, b, y, stream):
     _lib.check(_lib.load().sdmrg_axpby(x.numel(), float(a), x.data_ptr(), float(b),
                                        y.data_ptr(), stream))
+
+
+def _lowest_ritz(alphas, betas):
+    if len(alphas) == 1:
+        return float(alphas[0]), np.ones(1)
+    w, v = eigh_tridiagonal(np.asarray(alphas), np.asarray(betas), select="i",
+                            select_range=(0, 0))
+    return float(w[0]), v[:, 0]
 
 
 def lanczos_ground(apply_op, guess, tol=1e-12, max_iter=200):
@@ -139,18 +161,15 @@ def lanczos_ground(apply_op, guess, tol=1e-12, max_iter=200):
             total_iter += 1
             coef = basis.project_out(w, stream)                 # pass 1 (alpha)
             scal[1:2].copy_(coef[basis.count - 1:basis.count])
-            basis.project_out(w, stream)                        # pass 2
-            _nrm2(w, scal[2:3], stream)
+            basis.project_out(w, stream, norm_out=scal[2:3])    # pass 2 + ||w||
             host = scal.cpu().numpy()                           # one D2H per step
             alphas.append(float(host[1]))
             beta = float(host[2])
-            tri = np.diag(alphas)
-            if betas:
-                off = np.diag(betas, 1)
-                tri = tri + off + off.T
-            evals, evecs = np.linalg.eigh(tri)                  # dmrg.py:76
-            energy = float(evals[0])
-            ritz = evecs[:, 0]
+            # dmrg.py:76 eigh of the k x k tridiagonal: only its lowest pair
+            # is used, so the O(k^2) tridiagonal solver (LAPACK stebz/stein)
+            # replaces the dense O(k^3) eigh — same Ritz pair to rounding, and
+            # no k = 300 dense solve per iteration on the host
+            energy, ritz = _lowest_ritz(alphas, betas)
             est = abs(beta * ritz[-1])
             if est <= 0.1 * tol * (1.0 + abs(energy)) or beta < 1e-14 \
                     or basis.count == dim:                      # dmrg.py:81

@@ -95,7 +95,9 @@ def test_sigma_subset_L30_D1024_paths(fused):
     assert (stats["fused_outs"] > 0) == fused
 
 
-def test_sigma_subset_L76_D4096():
-    """CAS(113,76)-sized partition (north-star workload): fused kernel."""
-    stats, ng = _check(76, 4096, 0.03, seed=7, n_elec=113)
-    assert ng > 1000 and stats["fused_outs"] > 0
+@pytest.mark.parametrize("fused", [False, True])
+def test_sigma_subset_L76_D4096(fused):
+    """CAS(113,76)-sized partition (north-star workload): the two-phase
+    engine (default) and the fused small-sector kernel (SDMRG_FUSED=1)."""
+    stats, ng = _check(76, 4096, 0.03, seed=7, n_elec=113, fused=fused)
+    assert ng > 1000 and (stats["fused_outs"] > 0) == fused

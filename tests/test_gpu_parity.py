@@ -50,6 +50,20 @@ def test_plan_apply_matches_reference_sigma(golden):
     assert plan.stats["ref_flops"] == int(pi.meta["ref_flops"])
 
 
+def test_fused_kernel_matches_reference_sigma(golden, monkeypatch):
+    """The fused small-sector kernel (SDMRG_FUSED=1: T = psi R^T chained in
+    registers) on the reference's golden partitions, bitwise repeatable."""
+    from paper_2305_05581_b200.plan import DevicePlan
+    name, pi = golden
+    monkeypatch.setenv("SDMRG_FUSED", "1")
+    plan = DevicePlan(pi)
+    assert plan.stats["fused_outs"] > 0
+    psi = torch.from_numpy(pi.meta["psi"]).cuda()
+    sigma = plan.apply(psi).clone()
+    assert rel_err(sigma.cpu().numpy(), pi.meta["sigma"]) <= 1e-12
+    assert torch.equal(plan.apply(psi), sigma)
+
+
 def test_plan_apply_accumulates(golden):
     from paper_2305_05581_b200.plan import DevicePlan
     name, pi = golden
@@ -405,3 +419,27 @@ def test_engine_variants_bitwise_equal(monkeypatch, stack):
     assert torch.equal(outs[0], outs[1])
     ref = heff.apply_groups(pi, heff.build_groups(pi), psi)
     assert rel_err(outs[0].numpy(), ref) <= 1e-12
+
+
+def test_krylov_project_multislab():
+    """sdmrg_krylov_project (one CGS pass over all Krylov slabs, fused norm)
+    against the same projection in torch, k spanning three 32-vector slabs."""
+    from paper_2305_05581_b200 import _lib
+    lib = _lib.load()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    n, k = 10007, 70
+    slabs = [torch.randn(32, n, generator=g, dtype=torch.float64, device="cuda") for _ in range(3)]
+    v = torch.cat(slabs)[:k]
+    w = torch.randn(n, generator=g, dtype=torch.float64, device="cuda")
+    coef = torch.zeros(k, dtype=torch.float64, device="cuda")
+    nrm = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ref_c = v @ w
+    ref_w = w - v.T @ ref_c
+    ptrs = (_lib.c_vp * 3)(*[s.data_ptr() for s in slabs])
+    stream = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.sdmrg_krylov_project(3, ptrs, 32, k, n, w.data_ptr(), coef.data_ptr(),
+                                        nrm.data_ptr(), stream))
+    torch.cuda.synchronize()
+    assert torch.allclose(coef, ref_c, rtol=1e-12, atol=1e-9)
+    assert torch.allclose(w, ref_w, rtol=1e-10, atol=1e-9)
+    assert abs(nrm.item() - ref_w.norm().item()) <= 1e-10 * ref_w.norm().item()

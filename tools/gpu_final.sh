@@ -1,8 +1,22 @@
 #!/bin/bash
-# End-of-round call: the round script + the D sweep + the reference arm line
+# Round-end GPU pass: smoke, the whole -m gpu suite, the bench line and the
+# reference arm, the ncu launch list of the bench command, one full ncu
+# capture of each engine phase at the bench workload (L=50 D=4096), the
+# cuobjdump SASS opcode summary of the shipped library.  tools/gpu_final.sh TAG
 TAG=${1:-final}
-bash tools/gpu_round.sh $TAG
 OUT=gpurun_out/$TAG
-timeout 1200 python tools/d_sweep.py 30 512,1024,2048,4096,8192 $OUT/d_sweep.jsonl > $OUT/d_sweep.log 2>&1
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
-tail -c 400 $OUT/bench_reference.json
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $OUT/gpu.txt 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+if [ "$2" != "skip-tests" ]; then
+  timeout 2400 python -m pytest tests -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+fi
+timeout 1200 python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --scale "" --sweep "" > $OUT/bench_under_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_gemm_kernel -s 2 -c 1 \
+    -o $OUT/prof_p1 python tools/prof_apply.py 50 4096 2 > $OUT/ncu_p1.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_gemm_kernel -s 3 -c 1 \
+    -o $OUT/prof_p2 python tools/prof_apply.py 50 4096 2 > $OUT/ncu_p2.log 2>&1
+ls -la $OUT
