@@ -435,17 +435,40 @@ def density_matrix(psi, side, fused, device):
     return {q: rbuf[roff[q]:roff[q] + fdims[q] ** 2].view(fdims[q], fdims[q]) for q in sectors}
 
 
+def _sector_eigh(mats, engine):
+    """Eigenpairs of every ρ sector, descending: sectors of equal dimension
+    go to the eigensolver as ONE batched call, and all eigenvalues come back
+    to the host in one transfer (one eigh + one sync per sector was ~0.3 s
+    per renormalization at L=16 D=256)."""
+    by_dim = {}
+    for q, mat in mats.items():
+        by_dim.setdefault(int(mat.shape[0]), []).append(q)
+    vals, vecs = {}, {}
+    for n, qs in by_dim.items():
+        if len(qs) == 1:
+            ev, vc = engine.eigh(mats[qs[0]])
+            vals[qs[0]], vecs[qs[0]] = ev.flip(0), vc.flip(1)
+            continue
+        ev, vc = engine.eigh(torch.stack([mats[q] for q in qs]))
+        for k, q in enumerate(qs):
+            vals[q], vecs[q] = ev[k].flip(0), vc[k].flip(1)
+    order = list(mats)
+    flat = torch.cat([vals[q] for q in order]).cpu().numpy() if order else np.zeros(0)
+    scores, pos = {}, 0
+    for q in order:
+        n = int(vals[q].shape[0])
+        scores[q] = flat[pos:pos + n]
+        pos += n
+    return scores, vecs
+
+
 def renormalize(model, psi, side, old_store, site_index, d_max, engine):
     """dmrg.py:335 renormalize: enlarge, ρ eigensystem (dmrg.py:221), top-D
     (dmrg.py:204), W^T O W of every maintained operator (dmrg.py:254)."""
     dev = engine.device
     fused, keys, terms, comp_defs = enlarge_spec(model, old_store, site_index, dev)
     rho = density_matrix(psi, side, fused, dev)
-    scores, vecs = {}, {}
-    for q, mat in rho.items():
-        evals, evecs = engine.eigh(mat)
-        scores[q] = evals.flip(0).cpu().numpy()
-        vecs[q] = evecs.flip(1)
+    scores, vecs = _sector_eigh(rho, engine)
     info = {}
     kept = select_states(scores, d_max, info)
     total = sum(float(np.sum(v)) for v in scores.values())
