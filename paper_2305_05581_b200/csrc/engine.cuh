@@ -654,9 +654,39 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const double* gmem, i
 __device__ __forceinline__ void cp_async16_full(uint32_t saddr, const double* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
 }
-template <bool KCONTIG, int NC_LD, int CAP>
+// SDMRG_L2HINT: L2 eviction priority per operand (createpolicy +
+// cp.async ...L2::cache_hint): the streamed-once operand (phase 2: T,
+// written by phase 1 and read by ~1.1 groups) evict-first, the re-used one
+// (the operator blocks, each read by many products) evict-last.
+#ifndef SDMRG_L2HINT
+#define SDMRG_L2HINT 0
+#endif
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t p;
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_async16_hint(uint32_t saddr, const double* gmem, int src_bytes,
+                                                uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(saddr),
+               "l"(gmem), "r"(src_bytes), "l"(pol));
+}
+template <bool HINT>
+__device__ __forceinline__ void cp16(uint32_t saddr, const double* gmem, int src_bytes, uint64_t pol) {
+  if (HINT) cp_async16_hint(saddr, gmem, src_bytes, pol);
+  else cp_async16(saddr, gmem, src_bytes);
+}
+template <bool HINT>
+__device__ __forceinline__ void cp16_full(uint32_t saddr, const double* gmem, uint64_t pol) {
+  if (HINT) cp_async16_hint(saddr, gmem, 16, pol);
+  else cp_async16_full(saddr, gmem);
+}
+
+template <bool KCONTIG, int NC_LD, int CAP, bool HINT = false>
 __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const double* src, int ld,
-                                                     int extent, int krem, int lane) {
+                                                     int extent, int krem, int lane,
+                                                     uint64_t pol = 0) {
   if (KCONTIG) {
     const int k = 2 * (lane & 7), r0 = lane >> 3;
     const double* p = src + (int64_t)r0 * ld + k;
@@ -665,13 +695,13 @@ __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const doubl
     const int nrow = (extent - r0 + 3) >> 2;
     if (k + 1 < krem) {
 #pragma unroll 4
-      for (int i = 0; i < nrow; ++i) cp_async16_full(s0 + i * (4 * KC_LD * 8), p + (int64_t)(4 * i) * ld);
+      for (int i = 0; i < nrow; ++i) cp16_full<HINT>(s0 + i * (4 * KC_LD * 8), p + (int64_t)(4 * i) * ld, pol);
     } else {
       const int bytes = k < krem ? 8 : 0;
       const double* q = k < krem ? p : src;
       const int64_t step = k < krem ? 4 * (int64_t)ld : 0;
 #pragma unroll 4
-      for (int i = 0; i < nrow; ++i) cp_async16(s0 + i * (4 * KC_LD * 8), q + i * step, bytes);
+      for (int i = 0; i < nrow; ++i) cp16<HINT>(s0 + i * (4 * KC_LD * 8), q + i * step, bytes, pol);
     }
   } else {
 #pragma unroll
@@ -682,12 +712,12 @@ __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const doubl
         const uint32_t s0 = sbase + c * 8;
         if (krem >= BK) {
 #pragma unroll
-          for (int k = 0; k < BK; ++k) cp_async16_full(s0 + k * (NC_LD * 8), p + (int64_t)k * ld);
+          for (int k = 0; k < BK; ++k) cp16_full<HINT>(s0 + k * (NC_LD * 8), p + (int64_t)k * ld, pol);
         } else {
 #pragma unroll
           for (int k = 0; k < BK; ++k)
-            cp_async16(s0 + k * (NC_LD * 8), k < krem ? p + (int64_t)k * ld : src,
-                       k < krem ? 16 : 0);
+            cp16<HINT>(s0 + k * (NC_LD * 8), k < krem ? p + (int64_t)k * ld : src,
+                       k < krem ? 16 : 0, pol);
         }
       }
     }
@@ -806,6 +836,14 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
   };
   int stage = 0;
   uint32_t phase = 0;
+  // phase 1 (TB): A = ψ (small, L2-resident), B = right operator blocks
+  // (re-used by every ψ key of their sector); phase 2: A = operator blocks /
+  // pre-sums (re-used), B = T (streamed)
+  uint64_t pol_a = 0, pol_b = 0;
+  if (SDMRG_L2HINT) {
+    pol_a = l2_policy(true);
+    pol_b = l2_policy(TB);
+  }
   // Tile queue with two tiles of lookahead: the index of tile i+2 is claimed
   // while tile i streams and its descriptor is loaded at the end of tile i, so
   // neither the atomic nor the dependent descriptor load sits on the path
@@ -969,8 +1007,11 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
           }
           if (load_a) load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
         } else if (BULK) {
-          if (load_a) load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
-          if (load_b) load_operand_aligned<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
+          constexpr bool H = SDMRG_L2HINT != 0;
+          if (load_a)
+            load_operand_aligned<!TA, NC_LD_A, BM, H>(sa, asrc, sg.lda, cur.tm, krem, lane, pol_a);
+          if (load_b)
+            load_operand_aligned<TB, NC_LD_B, BN, H>(sb, bsrc, sg.ldb, cur.tn, krem, lane, pol_b);
         } else {
           if (load_a) load_operand_async<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
           if (load_b) load_operand_async<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
