@@ -87,13 +87,15 @@ struct Tile {        // host only
 };
 // Device form of a tile: the problem fields folded in, so the producer needs
 // one dependent load (tile -> segment) instead of two.
-struct TileRec {     // 40 B
+struct TileRec {     // 48 B
   uint64_t c;        // handle of C(0,0) of the problem
   int32_t ldc, beta;
   int32_t seg_begin, seg_end;
   int32_t row0, col0;
   int16_t tm, tn;
   int32_t colw;      // column-tile width of the problem (stage-tiled B)
+  int32_t sib_slot;  // SDMRG_LOCKSTEP: first progress slot of the problem's tiles
+  int16_t nsib, sib; // tiles of the problem, this tile's index among them
 };
 struct Seg {         // 40 B
   uint64_t a;        // handle of opA(0,0)
@@ -124,6 +126,9 @@ struct Seg {         // 40 B
 // number of 8-row (8-column) blocks, so the four DMMA warps stay balanced
 #ifndef SDMRG_ROTATE
 #define SDMRG_ROTATE 1
+#endif
+#ifndef SDMRG_LOCKSTEP
+#define SDMRG_LOCKSTEP 0
 #endif
 #ifndef SDMRG_GRID_ADAPT
 #define SDMRG_GRID_ADAPT 1
@@ -881,11 +886,35 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
       }
       if (next < ntiles && nrec.seg_begin < nrec.seg_end) sn = segs[nrec.seg_begin];
     }
+    // SDMRG_LOCKSTEP: the tiles of one σ problem read the same operand
+    // panels (row siblings the same A rows, column siblings the same B
+    // columns); a producer more than SDMRG_LOCKSTEP segments ahead of a
+    // started, unfinished sibling waits for it, so the shared panels are
+    // read while still in L2.  The slowest sibling never waits: no deadlock,
+    // and the data flow is untouched (timing only).
+    volatile int* prog = reinterpret_cast<volatile int*>(sbases[kMaxBases - 1]);
+    const bool lock = SDMRG_LOCKSTEP > 0 && prog != nullptr && cur.nsib > 1;
+    if (lock && lane == 0) prog[cur.sib_slot + cur.sib] = 1;
     bool first = true;
     int kfill = 0;           // packed rows in the open stage (multiple of 4)
     double open_scale = 1.0; // SDMRG_PACK == 2: the open stage's (uniform) scale
     bool unit = true;        // every k4 step of the open stage unscaled
     for (int s = cur.seg_begin; s < cur.seg_end; ++s) {
+      if (lock) {
+        const int k = s - cur.seg_begin;
+        if (lane == 0) {
+          prog[cur.sib_slot + cur.sib] = k + 1;
+          for (int j = 0; j < cur.nsib; ++j) {
+            if (j == cur.sib) continue;
+            int v = prog[cur.sib_slot + j];
+            while (v >= 1 && v < (1 << 30) && v - 1 < k - SDMRG_LOCKSTEP) {
+              __nanosleep(256);
+              v = prog[cur.sib_slot + j];
+            }
+          }
+        }
+        __syncwarp();
+      }
       const Seg sg = sn;
       if (s + 1 < cur.seg_end) {
         sn = segs[s + 1];
@@ -1027,6 +1056,7 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
         }
       }
     }
+    if (lock && lane == 0) prog[cur.sib_slot + cur.sib] = 1 << 30;  // finished
     t2 = __shfl_sync(0xffffffffu, t2, 0);
     share(t2, 0);
     TileRec n2{};

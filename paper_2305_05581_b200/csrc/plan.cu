@@ -182,6 +182,7 @@ struct sdmrg_plan {
   cudaEvent_t fork = nullptr, join = nullptr;
   sdmrg_plan_stats stats{};
   int64_t fused_outs = 0;          // σ problems on the fused kernel
+  int* progress = nullptr;         // phase-2 sibling progress slots (SDMRG_LOCKSTEP)
   double shard_balance = 1.0;      // mean / max rank load (world > 1)
   int timing = 0;
 };
@@ -1120,11 +1121,13 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   if (!rc && !plan->chunks.empty())
     rc = cuda_check(cudaMalloc(&plan->counters, sizeof(int) * 3 * plan->chunks.size()),
                     "cudaMalloc counters");
+  int64_t max_slots = 0;
   for (auto& ch : plan->chunks) {
     if (rc) break;
     rc = ch.host1.upload(&ch.p1, 0);
     if (!rc) rc = ch.host2.upload(&ch.p2, 0);
     if (!rc) rc = ch.fused.upload();
+    max_slots = std::max(max_slots, ch.p2.nslots);
     for (CombList* cl : {&ch.comb0, &ch.comb3}) {
       if (!rc) rc = upload_vec(cl->tasks, &cl->d_tasks);
       if (!rc) rc = upload_vec(cl->outs, &cl->d_outs);
@@ -1137,6 +1140,8 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     ch.host1 = GemmBatch();
     ch.host2 = GemmBatch();
   }
+  if (!rc && SDMRG_LOCKSTEP > 0 && max_slots > 0)
+    rc = cuda_check(cudaMalloc(&plan->progress, sizeof(int) * max_slots), "cudaMalloc progress");
   if (rc) {
     sdmrg_plan_destroy(plan);
     return rc;
@@ -1273,7 +1278,14 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (plan->timing) cudaEventRecord(ch.ev[3], stream);
     if (fork) cudaStreamWaitEvent(stream, plan->join, 0);
     if (plan->timing) cudaEventRecord(ch.ev[4], stream);
-    rc = launch_engine(false, false, ch.p2, bases, plan->counters + 3 * c + 1, stream, true,
+    Bases b2 = bases;
+    if (plan->progress && ch.p2.nslots > 0) {
+      rc = cuda_check(cudaMemsetAsync(plan->progress, 0, sizeof(int) * ch.p2.nslots, stream),
+                      "memset progress");
+      if (rc) return rc;
+      b2.p[kMaxBases - 1] = reinterpret_cast<double*>(plan->progress);
+    }
+    rc = launch_engine(false, false, ch.p2, b2, plan->counters + 3 * c + 1, stream, true,
                        ch.p2_one_body);
     if (rc) return rc;
     rc = launch_fused(ch.fused, bases, plan->counters + 3 * c + 2, stream);
@@ -1358,6 +1370,7 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
   if (plan->join) cudaEventDestroy(plan->join);
   if (plan->side) cudaStreamDestroy(plan->side);
   if (plan->counters) cudaFree(plan->counters);
+  if (plan->progress) cudaFree(plan->progress);
   delete plan;
   return SDMRG_OK;
 }

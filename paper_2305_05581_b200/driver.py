@@ -838,6 +838,11 @@ def _iterate(state, position, d_max, schedule, sweep_index, direction):
     _sync(dev)
     t2 = time.perf_counter()
     tim["aux_s"] = t2 - t1
+    if dev.type == "cuda":
+        # the plan sizes its T workspace from the driver's free HBM: hand
+        # torch's cached-but-unused blocks back first (L=30 D=2048 ran out of
+        # memory with 55 GB held in torch's cache)
+        torch.cuda.empty_cache()
     plan = eng.plan(pi, al, ar)
     del al, ar, comp_l, comp_r
     if plan.psi_size != struct.size:

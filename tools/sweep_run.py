@@ -10,6 +10,8 @@ energy differences up to the first degenerate-multiplet cut.
 import argparse
 import json
 import os
+
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 import sys
 import time
 
