@@ -1140,7 +1140,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     ch.host1 = GemmBatch();
     ch.host2 = GemmBatch();
   }
-  if (!rc && SDMRG_LOCKSTEP > 0 && max_slots > 0)
+  if (!rc && SDMRG_LOCKSTEP > 0 && max_slots > 0 && !getenv("SDMRG_NO_LOCK"))
     rc = cuda_check(cudaMalloc(&plan->progress, sizeof(int) * max_slots), "cudaMalloc progress");
   if (rc) {
     sdmrg_plan_destroy(plan);
