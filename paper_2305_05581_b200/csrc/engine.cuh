@@ -110,8 +110,16 @@ struct Seg {         // 40 B
   double scale;
 };
 
+// SDMRG_BIG: 128 x 128 tiles, 16 DMMA warps (4 x 4 grid of <= 32 x 32 warp
+// tiles) and 2 producer warps, one CTA per SM — the phase-2 instance for σ
+// blocks of 65..128 rows and columns, whose four 64 x 64 tiles would each
+// stream their own copy of the shared row / column operand panels
+// (compiled as a second instance in engine_big.cu, namespace sdmrg_big)
+#ifndef SDMRG_BIG
+#define SDMRG_BIG 0
+#endif
 #ifndef SDMRG_STAGES
-#define SDMRG_STAGES (SDMRG_WIDE ? 4 : 3)
+#define SDMRG_STAGES (SDMRG_BIG ? 5 : (SDMRG_WIDE ? 4 : 3))
 #endif
 #ifndef SDMRG_TILE
 #define SDMRG_TILE 64
@@ -158,7 +166,7 @@ __host__ __device__ constexpr bool grid_adapt() {
 #define SDMRG_LDS128 0
 #endif
 #ifndef SDMRG_MINB
-#define SDMRG_MINB ((SDMRG_TILE > 64 || SDMRG_WIDE) ? 2 : 4)
+#define SDMRG_MINB (SDMRG_BIG ? 1 : ((SDMRG_TILE > 64 || SDMRG_WIDE) ? 2 : 4))
 #endif
 // SDMRG_WIDE: 64 x 128 tiles, 8 DMMA warps (2 x 4 grid of <= 32 x 32 warp
 // tiles) per CTA, 2 CTAs per SM — the same 16 DMMA warps per SM as the
@@ -169,12 +177,13 @@ __host__ __device__ constexpr bool grid_adapt() {
 constexpr int BM = SDMRG_TILE, BN = SDMRG_WIDE ? 2 * SDMRG_TILE : SDMRG_TILE, BK = 16;
 constexpr int STAGES = SDMRG_STAGES;
 constexpr int MAXB = BM / 16;                    // 8x8 blocks per warp and dimension
-static_assert(BM == 64 || BM == 96, "tile edge 64 or 96");
-constexpr int WGRID_R = 2, WGRID_C = SDMRG_WIDE ? 4 : 2, CONSUMERS = WGRID_R * WGRID_C;
+static_assert(BM == 64 || BM == 96 || (SDMRG_BIG && BM == 128), "tile edge 64, 96 (or 128 big)");
+constexpr int WGRID_R = SDMRG_BIG ? 4 : 2, WGRID_C = (SDMRG_WIDE || SDMRG_BIG) ? 4 : 2,
+              CONSUMERS = WGRID_R * WGRID_C;
 // SDMRG_PRODUCERS=2: one producer warp per operand (A loader leads the tile
 // queue, the B loader follows through shared memory and a named barrier)
 #ifndef SDMRG_PRODUCERS
-#define SDMRG_PRODUCERS 1
+#define SDMRG_PRODUCERS (SDMRG_BIG ? 2 : 1)
 #endif
 constexpr int PRODUCERS = SDMRG_PRODUCERS;
 static_assert(PRODUCERS == 1 || PRODUCERS == 2, "one or two producer warps");
@@ -579,7 +588,7 @@ __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring&
     }
   }
   switch (mblk * 8 + nblk) {
-#if SDMRG_TILE > 64
+#if SDMRG_TILE > 64 && !SDMRG_BIG
     SDMRG_TILE_CASE(6, 6) SDMRG_TILE_CASE(6, 5) SDMRG_TILE_CASE(5, 6) SDMRG_TILE_CASE(5, 5)
     SDMRG_TILE_CASE(6, 4) SDMRG_TILE_CASE(6, 3) SDMRG_TILE_CASE(6, 2) SDMRG_TILE_CASE(6, 1)
     SDMRG_TILE_CASE(5, 4) SDMRG_TILE_CASE(5, 3) SDMRG_TILE_CASE(5, 2) SDMRG_TILE_CASE(5, 1)
@@ -1074,7 +1083,9 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
 // BULK ("aligned"): every operand block 16-byte aligned with even leading
 // dimensions (the H_eff plan's padded layouts) -> 16-byte cp.async; the
 // launcher selects it per batch.
-#if SDMRG_TILE > 64
+#if SDMRG_BIG
+#define SDMRG_KERNEL_BOUNDS __launch_bounds__(THREADS, 1)
+#elif SDMRG_TILE > 64
 #define SDMRG_KERNEL_BOUNDS __maxnreg__(200)
 #else
 #define SDMRG_KERNEL_BOUNDS __launch_bounds__(THREADS, SDMRG_MINB)
@@ -1147,10 +1158,19 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
       wc0 = 0;
       mblk = mb >> 2;
       wr0 = 8 * mblk * cw_index(wr, wc);
-    } else {
+    } else if (WGRID_R == 2) {
       const int mb0 = (mb + 1) >> 1;
       mblk = wr == 0 ? mb0 : mb - mb0;
       wr0 = wr == 0 ? 0 : mb0 * 8;
+      // columns: balanced over WGRID_C warps
+      const int nbase = nb / WGRID_C, nextra = nb - nbase * WGRID_C;
+      nblk = nbase + (wc < nextra ? 1 : 0);
+      wc0 = 8 * (wc * nbase + min(wc, nextra));
+    } else {
+      // rows and columns balanced over the WGRID_R x WGRID_C grid
+      const int mbase = mb / WGRID_R, mextra = mb - mbase * WGRID_R;
+      mblk = mbase + (wr < mextra ? 1 : 0);
+      wr0 = 8 * (wr * mbase + min(wr, mextra));
       // columns: balanced over WGRID_C warps
       const int nbase = nb / WGRID_C, nextra = nb - nbase * WGRID_C;
       nblk = nbase + (wc < nextra ? 1 : 0);

@@ -34,7 +34,20 @@
 
 using namespace sdmrg;
 
+extern "C" int sdmrg_internal_launch_big(const void* tiles, int ntiles, const void* segs,
+                                         int* counter, const void* bases, void* stream,
+                                         int one_body);
+extern "C" int sdmrg_internal_big_grid();
+
 namespace {
+
+// Phase-2 σ blocks of 65..128 rows and columns on the 128 x 128 big-tile
+// engine instance (SDMRG_BIG=1; default off until measured faster).
+bool big_tiles_enabled() {
+  const char* e = getenv("SDMRG_BIG");
+  return e && e[0] == '1';
+}
+inline bool big_problem(int q, int r) { return q > 64 && q <= 128 && r > 64 && r <= 128; }
 
 // Engine bases.  The engine's bulk-copy producer needs 16-byte aligned
 // operand rows, so the plan keeps padded copies of everything it reads
@@ -129,6 +142,9 @@ struct CombList {
 struct Chunk {
   GemmBatch host1, host2;  // released after upload
   DeviceBatch p1, p2;
+  GemmBatch host2big;      // phase 2, σ blocks of 65..128 x 65..128 (engine_big.cu)
+  DeviceBatch p2big;
+  bool p2big_one_body = false;
   FusedBatch fused;        // small-sector σ problems on the fused kernel (fused.cuh)
   CombList comb0;          // phase 0: pre-summed left operators
   CombList comb3;          // phase 3: split-K partial sums into σ
@@ -951,28 +967,38 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     // (σ first, then parts 0..S-1: deterministic, no atomics).  Fused σ
     // problems use the same rule against the fused kernel's grid.
     auto tiles_of = [](int extent) { return (extent + BM - 1) / BM; };
-    double total_cost = 0.0, total_fcost = 0.0;
+    const bool big_on = big_tiles_enabled();
+    double total_cost = 0.0, total_fcost = 0.0, total_bcost = 0.0;
     for (const OutProb& op : outs) {
       if (!op.fsegs.empty()) total_fcost += op.fcost;
+      else if (big_on && big_problem(op.q, op.r)) total_bcost += double(op.q) * op.r * op.ksum;
       else total_cost += double(op.q) * op.r * op.ksum;
     }
     const double granule = std::max(
         total_cost / (double(d->dry_run ? 1 : engine_grid(false, false)) * split_factor()) + 1.0,
         split_min());
+    const double bgranule = std::max(
+        total_bcost / (double(d->dry_run ? 148 : sdmrg_internal_big_grid()) * split_factor()) + 1.0,
+        split_min());
+    ch.host2big.cap = 128;
     const double fgranule =
         total_fcost / (double(d->dry_run ? 148 : fused_grid_size()) * split_factor()) + 1.0;
     for (const OutProb& op : outs) {
       const bool fz = !op.fsegs.empty();
+      const bool bg = !fz && big_on && big_problem(op.q, op.r);
+      GemmBatch& h2 = bg ? ch.host2big : ch.host2;
       const size_t nseg = fz ? op.fsegs.size() : op.segs.size();
       double tile_cost;
-      if (fz) {
+      if (bg) {
+        tile_cost = double(op.q) * op.r * op.ksum;
+      } else if (fz) {
         const int rb = (op.r + 7) / 8;
         tile_cost = op.fcost * std::min(rb, F_RT) / rb;  // the widest column tile's share
       } else {
         tile_cost = double(op.q) / tiles_of(op.q) * (double(op.r) / tiles_of(op.r)) * op.ksum;
       }
-      int nsplit = static_cast<int>(std::min<double>(std::ceil(tile_cost / (fz ? fgranule : granule)),
-                                                     double(nseg)));
+      int nsplit = static_cast<int>(std::min<double>(
+          std::ceil(tile_cost / (fz ? fgranule : (bg ? bgranule : granule))), double(nseg)));
       nsplit = std::max(nsplit, 1);
       const uint64_t sig = make_handle(B_SIGMA, plan->offs[op.o]);
       auto emit = [&](uint64_t c, int beta, size_t s0, size_t s1) {
@@ -981,12 +1007,12 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
           ch.fused.segs.insert(ch.fused.segs.end(), op.fsegs.begin() + s0, op.fsegs.begin() + s1);
           ch.fused.add_problem(c, op.r, op.q, op.r, beta, fb);
         } else {
-          ch.host2.begin_prob(c, op.r, op.q, op.r, beta);
+          h2.begin_prob(c, op.r, op.q, op.r, beta);
           for (size_t x = s0; x < s1; ++x) {
             const Seg& sg = op.segs[x];
-            ch.host2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale, sg.btile);
+            h2.add_seg(sg.a, sg.lda, sg.b, sg.ldb, sg.k, sg.scale, sg.btile);
           }
-          ch.host2.end_prob();
+          h2.end_prob();
         }
       };
       auto seg_k = [&](size_t x) { return fz ? op.fsegs[x].m : op.segs[x].k; };
@@ -1019,6 +1045,10 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     ch.host1.finalize_tiles(0, getenv("SDMRG_P1_BY_PROBLEM") != nullptr);
     ch.host2.finalize_tiles(p2_octaves(), getenv("SDMRG_P2_BY_PROBLEM") != nullptr);
     ch.p2_one_body = use_one_body(ch.host2);
+    ch.host2big.finalize_tiles(0, false);
+    ch.p2big_one_body = use_one_body(ch.host2big);
+    tiles += (int64_t)ch.host2big.tiles.size();
+    segments += (int64_t)ch.host2big.segs.size();
     ch.fused.finalize();
     tiles += (int64_t)ch.fused.tiles.size();
     segments += (int64_t)ch.fused.segs.size();
@@ -1119,13 +1149,14 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
                              "memset workspace");
   }
   if (!rc && !plan->chunks.empty())
-    rc = cuda_check(cudaMalloc(&plan->counters, sizeof(int) * 3 * plan->chunks.size()),
+    rc = cuda_check(cudaMalloc(&plan->counters, sizeof(int) * 4 * plan->chunks.size()),
                     "cudaMalloc counters");
   int64_t max_slots = 0;
   for (auto& ch : plan->chunks) {
     if (rc) break;
     rc = ch.host1.upload(&ch.p1, 0);
     if (!rc) rc = ch.host2.upload(&ch.p2, 0);
+    if (!rc) rc = ch.host2big.upload(&ch.p2big, 0);
     if (!rc) rc = ch.fused.upload();
     max_slots = std::max(max_slots, ch.p2.nslots);
     for (CombList* cl : {&ch.comb0, &ch.comb3}) {
@@ -1139,6 +1170,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     }
     ch.host1 = GemmBatch();
     ch.host2 = GemmBatch();
+    ch.host2big = GemmBatch();
   }
   if (!rc && SDMRG_LOCKSTEP > 0 && max_slots > 0 && !getenv("SDMRG_NO_LOCK"))
     rc = cuda_check(cudaMalloc(&plan->progress, sizeof(int) * max_slots), "cudaMalloc progress");
@@ -1164,7 +1196,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   st.workspace_doubles = ws_max;
   int64_t kernels = 0;
   for (auto& ch : plan->chunks)
-    kernels += (ch.comb0.ntasks > 0) + (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0) + (ch.fused.ntiles > 0) +
+    kernels += (ch.comb0.ntasks > 0) + (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0) + (ch.p2big.ntiles > 0) + (ch.fused.ntiles > 0) +
                (ch.comb3.ntasks > 0);
   st.kernels_per_apply = kernels;
   st.algo_bytes = static_cast<int64_t>(algo_bytes);
@@ -1230,7 +1262,7 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (rc) return rc;
   }
   if (plan->chunks.empty()) return SDMRG_OK;
-  rc = cuda_check(cudaMemsetAsync(plan->counters, 0, sizeof(int) * 3 * plan->chunks.size(), stream),
+  rc = cuda_check(cudaMemsetAsync(plan->counters, 0, sizeof(int) * 4 * plan->chunks.size(), stream),
                   "memset counters");
   if (rc) return rc;
   if (plan->psi_copy.n > 0) {
@@ -1273,7 +1305,7 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (plan->timing) cudaEventRecord(ch.ev[1], s0);
     if (fork) cudaEventRecord(plan->join, plan->side);
     if (plan->timing) cudaEventRecord(ch.ev[2], stream);
-    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 3 * c, stream, true);
+    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 4 * c, stream, true);
     if (rc) return rc;
     if (plan->timing) cudaEventRecord(ch.ev[3], stream);
     if (fork) cudaStreamWaitEvent(stream, plan->join, 0);
@@ -1285,10 +1317,18 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
       if (rc) return rc;
       b2.p[kMaxBases - 1] = reinterpret_cast<double*>(plan->progress);
     }
-    rc = launch_engine(false, false, ch.p2, b2, plan->counters + 3 * c + 1, stream, true,
+    rc = launch_engine(false, false, ch.p2, b2, plan->counters + 4 * c + 1, stream, true,
                        ch.p2_one_body);
     if (rc) return rc;
-    rc = launch_fused(ch.fused, bases, plan->counters + 3 * c + 2, stream);
+    rc = launch_fused(ch.fused, bases, plan->counters + 4 * c + 2, stream);
+    if (rc) return rc;
+    if (ch.p2big.ntiles > 0) {
+      rc = cuda_check(static_cast<cudaError_t>(sdmrg_internal_launch_big(
+                          ch.p2big.tiles, static_cast<int>(ch.p2big.ntiles), ch.p2big.segs,
+                          plan->counters + 4 * c + 3, &bases, stream, ch.p2big_one_body)),
+                      "big-tile engine launch");
+      count_launch();
+    }
     if (rc) return rc;
     if (plan->timing) {
       cudaEventRecord(ch.ev[5], stream);
@@ -1352,6 +1392,7 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
   for (auto& ch : plan->chunks) {
     ch.p1.release();
     ch.p2.release();
+    ch.p2big.release();
     ch.fused.release();
     ch.comb0.release();
     ch.comb3.release();

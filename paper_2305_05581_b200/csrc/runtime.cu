@@ -116,7 +116,7 @@ void GemmBatch::end_prob() {
     const int per = ((extent + nt - 1) / nt + 7) / 8 * 8;
     return std::max(per, 8);
   };
-  const int tm = split(p.m, BM), tn = split(p.n, BN);
+  const int tm = split(p.m, cap > 0 ? cap : BM), tn = split(p.n, cap > 0 ? cap : BN);
   for (int r0 = 0; r0 < p.m; r0 += tm)
     for (int c0 = 0; c0 < p.n; c0 += tn) {
       const int mm = std::min(tm, p.m - r0), nn = std::min(tn, p.n - c0);

@@ -30,6 +30,7 @@ struct DeviceBatch {
 
 // Host staging of problems/segments; tiles derived per problem.
 struct GemmBatch {
+  int cap = 0;          // tile edge (0: the default instance's BM x BN)
   std::vector<Prob> probs;
   std::vector<Seg> segs;
   std::vector<Tile> tiles;
