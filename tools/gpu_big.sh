@@ -17,3 +17,6 @@ for v in 1 0; do
   echo "[big=$v] 76 8192: $(SDMRG_BIG=$v timeout 900 python tools/quick.py 76 8192 113 2>&1 | tail -1)" | cut -c1-220 >> $OUT/ab.log
 done
 ls -la $OUT
+for ws in 11250000000 0; do
+  echo "[ws=$ws] 50 4096: $(SDMRG_WS=$ws timeout 600 python tools/quick.py 50 4096 2>&1 | tail -1)" | cut -c1-220 >> $OUT/ab.log
+done
