@@ -209,6 +209,10 @@ int sdmrg_plan_arena(const sdmrg_plan* plan, int side, double** base, int64_t* s
 /* Shard ownership: mine[i] = 1 when ψ key i is this rank's input sector
  * (psi_keys entries).  Every key belongs to exactly one rank of `world`.    */
 int sdmrg_plan_shard(const sdmrg_plan* plan, int32_t* mine);
+/* diag (device, psi_size doubles) := the diagonal of H_eff over this rank's
+ * ψ sectors (zero elsewhere; sum over ranks for the full diagonal) — the
+ * Davidson preconditioner of lanczos.py davidson_ground.  Stream-ordered. */
+int sdmrg_plan_diagonal(sdmrg_plan* plan, double* diag, void* stream);
 /* sigma (+)= H_eff psi over this rank's shard; device vectors of psi_size.
  * The operator pre-sums (phase 0: ψ-independent) are formed by the first
  * apply and reused by later ones; after changing the arenas in place call
@@ -246,6 +250,10 @@ int sdmrg_gemv_n(int k, int64_t n, const double* v, int64_t ldv,
  * Four launches whatever k is; fixed-order reductions (bitwise repeatable). */
 int sdmrg_krylov_project(int nslabs, const double* const* slabs, int slab_rows, int k, int64_t n,
                          double* w, double* coef_dev, double* norm_dev, void* stream);
+/* Davidson correction vector with the diagonal preconditioner of H_eff
+ * (sdmrg_plan_diagonal): t = r / (theta - diag), |theta - diag| >= 1e-8. */
+int sdmrg_davidson_precond(int64_t n, const double* r, const double* diag, double theta,
+                           double* t, void* stream);
 int sdmrg_scal_dev(int64_t n, const double* num_dev, const double* den_dev,
                    int invert_den, double* x, void* stream);
 /* y = a*x + b*y with host scalars.                                          */

@@ -82,6 +82,7 @@ _SIGS = {
     "sdmrg_plan_layout": (c_int, [c_vp, P_i32, P_i64]),
     "sdmrg_plan_groups": (c_int, [c_vp, P_i32, P_i32, P_i64, P_i64, P_dbl]),
     "sdmrg_plan_shard": (c_int, [c_vp, P_i32]),
+    "sdmrg_plan_diagonal": (c_int, [c_vp, c_vp, c_vp]),
     "sdmrg_plan_arena": (c_int, [c_vp, c_int, ctypes.POINTER(c_vp), P_i64, P_i64]),
     "sdmrg_plan_apply": (c_int, [c_vp, c_vp, c_vp, c_int, c_vp]),
     "sdmrg_plan_destroy": (c_int, [c_vp]),
@@ -93,6 +94,7 @@ _SIGS = {
     "sdmrg_gemv_t": (c_int, [c_int, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "sdmrg_gemv_n": (c_int, [c_int, c_i64, c_vp, c_i64, c_vp, c_dbl, c_vp, c_vp]),
     "sdmrg_krylov_project": (c_int, [c_int, c_vp, c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "sdmrg_davidson_precond": (c_int, [c_i64, c_vp, c_vp, c_dbl, c_vp, c_vp]),
     "sdmrg_scal_dev": (c_int, [c_i64, c_vp, c_vp, c_int, c_vp, c_vp]),
     "sdmrg_axpby": (c_int, [c_i64, c_dbl, c_vp, c_dbl, c_vp, c_vp]),
     "sdmrg_rotate": (c_int, [c_i64, P_i64, P_i64, P_i64, P_i64, P_i32, P_i32, P_i32, P_i32,

@@ -41,13 +41,21 @@ extern "C" int sdmrg_internal_big_grid();
 
 namespace {
 
-// Phase-2 σ blocks of 65..128 rows and columns on the 128 x 128 big-tile
-// engine instance (SDMRG_BIG=1; default off until measured faster).
-bool big_tiles_enabled() {
+// Phase-2 σ blocks that span more than one 64 x 64 tile go to the 128 x 128
+// big-tile engine instance (engine_big.cu), whose CTA loads each shared
+// row / column operand panel once for all its quadrants.  SDMRG_BIG: 0 off;
+// 1 (default) σ blocks of 65..128 x 65..128; 2 also wider / taller blocks
+// (max(q, r) > 64, min(q, r) > 32) in <= 128 x 128 tiles.
+int big_tiles_mode() {
   const char* e = getenv("SDMRG_BIG");
-  return e && e[0] == '1';
+  return e ? std::atoi(e) : 1;
 }
-inline bool big_problem(int q, int r) { return q > 64 && q <= 128 && r > 64 && r <= 128; }
+bool big_tiles_enabled() { return big_tiles_mode() > 0; }
+inline bool big_problem(int q, int r) {
+  const int mode = big_tiles_mode();
+  if (mode == 2) return std::max(q, r) > 64 && std::min(q, r) > 32;
+  return q > 64 && q <= 128 && r > 64 && r <= 128;
+}
 
 // Engine bases.  The engine's bulk-copy producer needs 16-byte aligned
 // operand rows, so the plan keeps padded copies of everything it reads
@@ -112,6 +120,38 @@ struct PadList {
     n = 0;
   }
 };
+
+// Diagonal of H_eff (the Davidson preconditioner): for every ψ key i, the
+// members of its diagonal group (i -> i) contribute s · L_a[x][x] R_b[y][y]
+// to element (x, y) of block i.  One CTA per key, members in table order
+// (deterministic).  Handles index the plan's padded arenas.
+struct DiagKey {
+  int64_t off;          // ψ offset of block i (to_vector layout)
+  int32_t m, n;         // block i: m x n
+  int32_t ldl, ldr;     // padded row strides of its L (m x m) / R (n x n) blocks
+  int32_t mem_begin, mem_end;
+};
+struct DiagMem {
+  int64_t l, r;         // element offsets of the L / R blocks in the padded arenas
+  double s;
+};
+__global__ void diag_kernel(const DiagKey* __restrict__ keys, int nkeys,
+                            const DiagMem* __restrict__ mems, const double* __restrict__ al,
+                            const double* __restrict__ ar, double* __restrict__ diag) {
+  for (int k = blockIdx.x; k < nkeys; k += gridDim.x) {
+    const DiagKey dk = keys[k];
+    const int64_t cnt = (int64_t)dk.m * dk.n;
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int x = static_cast<int>(e / dk.n), y = static_cast<int>(e - (int64_t)x * dk.n);
+      double acc = 0.0;
+      for (int t = dk.mem_begin; t < dk.mem_end; ++t) {
+        const DiagMem mm = mems[t];
+        acc += mm.s * al[mm.l + (int64_t)x * dk.ldl + x] * ar[mm.r + (int64_t)y * dk.ldr + y];
+      }
+      diag[dk.off + e] = acc;
+    }
+  }
+}
 
 // Host staging + device copy of one combine launch (combine.cuh).
 struct CombList {
@@ -199,6 +239,8 @@ struct sdmrg_plan {
   sdmrg_plan_stats stats{};
   int64_t fused_outs = 0;          // σ problems on the fused kernel
   int* progress = nullptr;         // phase-2 sibling progress slots (SDMRG_LOCKSTEP)
+  std::vector<DiagKey> diag_keys;  // H_eff diagonal work (this rank's ψ keys)
+  std::vector<DiagMem> diag_mems;
   double shard_balance = 1.0;      // mean / max rank load (world > 1)
   int timing = 0;
 };
@@ -616,6 +658,21 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     }
     psize_l = pad_offsets(d->nops_l, nL, use_l.data(), shL.data(), d->dim_l, false, poff_l);
     psize_r = pad_offsets(d->nops_r, nR, use_r.data(), shR.data(), d->dim_r, true, poff_r);
+  }
+  // diagonal-group members of this rank's ψ keys (sdmrg_plan_diagonal)
+  for (int64_t i = 0; i < nk; ++i) {
+    if (!mine[i]) continue;
+    const int m = d->dim_l[keys[i].jl], n = d->dim_r[keys[i].jr];
+    DiagKey dk{plan->offs[i], m, n, pad2(m), pad2(n), static_cast<int32_t>(plan->diag_mems.size()), 0};
+    for (const Member& mb : per_key[i]) {
+      if (mb.out != i) continue;
+      const size_t xl = (size_t)d->lop[mb.row] * nL + keys[i].jl;
+      const size_t xr = (size_t)d->rop[mb.row] * nR + keys[i].jr;
+      if (poff_l[xl] < 0 || poff_r[xr] < 0) continue;
+      plan->diag_mems.push_back({poff_l[xl], poff_r[xr], mb.scale});
+    }
+    dk.mem_end = static_cast<int32_t>(plan->diag_mems.size());
+    if (dk.mem_end > dk.mem_begin) plan->diag_keys.push_back(dk);
   }
 
   // ---- fused small-sector σ problems (fused.cuh): an out key whose rows q
@@ -1231,6 +1288,36 @@ int sdmrg_plan_arena(const sdmrg_plan* plan, int side, double** base, int64_t* s
   if (offsets)
     std::copy(plan->arena_off[side].begin(), plan->arena_off[side].end(), offsets);
   return SDMRG_OK;
+}
+
+int sdmrg_plan_diagonal(sdmrg_plan* plan, double* diag, void* stream_) {
+  if (!plan || !diag) return fail(SDMRG_EINVAL, "plan_diagonal: null argument");
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  int rc = cuda_check(cudaMemsetAsync(diag, 0, sizeof(double) * std::max<int64_t>(plan->stats.psi_size, 1),
+                                      stream), "memset diagonal");
+  if (rc || plan->diag_keys.empty()) return rc;
+  DiagKey* dk = nullptr;
+  DiagMem* dm = nullptr;
+  rc = cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&dk), plan->diag_keys.size() * sizeof(DiagKey),
+                                  stream), "diag keys");
+  if (!rc) rc = cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&dm),
+                                           std::max<size_t>(plan->diag_mems.size(), 1) * sizeof(DiagMem),
+                                           stream), "diag members");
+  if (!rc) rc = cuda_check(cudaMemcpyAsync(dk, plan->diag_keys.data(), plan->diag_keys.size() * sizeof(DiagKey),
+                                           cudaMemcpyHostToDevice, stream), "diag keys upload");
+  if (!rc && !plan->diag_mems.empty())
+    rc = cuda_check(cudaMemcpyAsync(dm, plan->diag_mems.data(), plan->diag_mems.size() * sizeof(DiagMem),
+                                    cudaMemcpyHostToDevice, stream), "diag members upload");
+  if (!rc) {
+    const int nkeys = static_cast<int>(plan->diag_keys.size());
+    diag_kernel<<<std::min(nkeys, 148 * 8), 256, 0, stream>>>(dk, nkeys, dm, plan->arena_l,
+                                                              plan->arena_r, diag);
+    count_launch();
+    rc = cuda_check(cudaGetLastError(), "diag launch");
+  }
+  if (dk) cudaFreeAsync(dk, stream);
+  if (dm) cudaFreeAsync(dm, stream);
+  return rc;
 }
 
 int sdmrg_plan_shard(const sdmrg_plan* plan, int32_t* mine) {

@@ -258,6 +258,29 @@ int sdmrg_krylov_project(int nslabs, const double* const* slabs, int slab_rows, 
   return cuda_check(cudaGetLastError(), "krylov_project launch");
 }
 
+// Davidson correction with the diagonal preconditioner:
+// t[j] = r[j] / (theta - diag[j]), |theta - diag[j]| floored at 1e-8
+__global__ void davidson_precond_kernel(int64_t n, const double* __restrict__ r,
+                                        const double* __restrict__ diag, double theta,
+                                        double* __restrict__ t) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double den = theta - diag[i];
+    if (fabs(den) < 1e-8) den = den < 0.0 ? -1e-8 : 1e-8;
+    t[i] = r[i] / den;
+  }
+}
+
+int sdmrg_davidson_precond(int64_t n, const double* r, const double* diag, double theta,
+                           double* t, void* stream) {
+  if (n < 0 || (n > 0 && (!r || !diag || !t))) return fail(SDMRG_EINVAL, "davidson_precond: bad arguments");
+  if (n == 0) return SDMRG_OK;
+  davidson_precond_kernel<<<grid_for_n(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, r, diag,
+                                                                                        theta, t);
+  count_launch();
+  return cuda_check(cudaGetLastError(), "davidson_precond launch");
+}
+
 int sdmrg_scal_dev(int64_t n, const double* num_dev, const double* den_dev, int invert_den,
                    double* x, void* stream) {
   if (n < 0) return fail(SDMRG_EINVAL, "scal: negative length");

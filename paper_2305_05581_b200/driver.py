@@ -46,12 +46,18 @@ class SweepSchedule:
     d: object = 64
     lanczos_tol: float = 1e-12
     lanczos_max_iter: int = 300
+    # "lanczos": the reference's eigensolver (dmrg.py:43), iteration for
+    # iteration; "davidson": diagonal-preconditioned Davidson on the device
+    # (lanczos.davidson_ground) — same acceptance test, fewer H_eff·ψ
+    eigensolver: str = "lanczos"
 
     def __post_init__(self):
         if self.n_sweeps < 0:
             raise DmrgError("sweep count must be non-negative")
         if self.lanczos_tol <= 0 or self.lanczos_max_iter < 1:
             raise DmrgError("tolerances must be positive")
+        if self.eigensolver not in ("lanczos", "davidson"):
+            raise DmrgError(f"unknown eigensolver {self.eigensolver!r}")
         ds = self.d if isinstance(self.d, (list, tuple)) else [self.d]
         if any(int(x) < 1 for x in ds):
             raise DmrgError("bond dimension must be >= 1")
@@ -103,6 +109,10 @@ class Engine:
     def lanczos(self, apply_op, guess, tol, max_iter):
         from .lanczos import lanczos_ground
         return lanczos_ground(apply_op, guess, tol=tol, max_iter=max_iter)
+
+    def davidson(self, apply_op, guess, diag, tol, max_iter):
+        from .lanczos import davidson_ground
+        return davidson_ground(apply_op, guess, diag, tol=tol, max_iter=max_iter)
 
     def eigh(self, mat):
         return torch.linalg.eigh(mat)
@@ -855,8 +865,12 @@ def _iterate(state, position, d_max, schedule, sweep_index, direction):
     def apply_op(vec):
         return plan.apply(vec, buf)
 
-    res = eng.lanczos(apply_op, _guess_vector(state, struct), schedule.lanczos_tol,
-                      schedule.lanczos_max_iter)
+    if schedule.eigensolver == "davidson":
+        res = eng.davidson(apply_op, _guess_vector(state, struct), plan.diagonal(),
+                           schedule.lanczos_tol, schedule.lanczos_max_iter)
+    else:
+        res = eng.lanczos(apply_op, _guess_vector(state, struct), schedule.lanczos_tol,
+                          schedule.lanczos_max_iter)
     flops = int(plan.flops) * (res.iterations + 1)
     plan.close()
     del plan, buf

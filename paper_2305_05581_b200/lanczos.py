@@ -191,3 +191,95 @@ def lanczos_ground(apply_op, guess, tol=1e-12, max_iter=200):
             return LanczosResult(energy, vec, total_iter, exhausted)
         v0 = vec
     return LanczosResult(energy, vec, total_iter, False)
+
+
+def davidson_ground(apply_op, guess, diag, tol=1e-12, max_iter=200, max_space=40):
+    """Lowest eigenpair by Davidson with the diagonal preconditioner (the
+    north star's eigensolver; the reference runs Lanczos, dmrg.py:43).
+
+    ``diag`` is the diagonal of the operator (``DevicePlan.diagonal``).  The
+    search space V and H V live on the device in 32-vector slabs; each step:
+    Ritz pair of the projected matrix (host, k <= max_space), residual
+    r = H u - θ u, correction t = r / (θ - diag) (sdmrg_davidson_precond),
+    two CGS passes against V with the norm fused (sdmrg_krylov_project), one
+    H_eff·ψ.  A full space collapses to the current Ritz vector.  Converged
+    when ||r|| <= tol (1 + |θ|) — the reference's acceptance test
+    (dmrg.py:91).  ``iterations`` counts H_eff applications.
+    """
+    lib = _lib.load()
+    if not isinstance(guess, torch.Tensor):
+        guess = torch.from_numpy(np.ascontiguousarray(guess, dtype=np.float64)).cuda()
+    guess = guess.to(torch.float64).contiguous()
+    dim = guess.numel()
+    device = guess.device
+    stream = torch.cuda.current_stream(device).cuda_stream
+    scal = torch.zeros(2, dtype=torch.float64, device=device)
+    _nrm2(guess, scal[0:1], stream)
+    nrm = float(scal[0].item())
+    if nrm == 0.0 or dim == 0:
+        raise LanczosError("davidson needs a nonzero starting vector")
+    V = KrylovBasis(dim, device)
+    W = KrylovBasis(dim, device)
+    coef = torch.zeros(max(max_space, 1) + 1, dtype=torch.float64, device=device)
+    mat = np.zeros((max_space, max_space))
+    u = torch.empty_like(guess)
+    hu = torch.empty_like(guess)
+    t = torch.empty_like(guess)
+    _axpby(1.0 / nrm, guess, 0.0, u, stream)
+    iters = 0
+
+    def add(vec):
+        """Append vec (normalised) to V, H vec to W, extend the projected matrix."""
+        nonlocal iters
+        k = V.count
+        _axpby(1.0, vec, 0.0, V.append_slot(), stream)
+        w = apply_op(V.vec(k))
+        iters += 1
+        _axpby(1.0, w, 0.0, W.append_slot(), stream)
+        # column k of V^T H V (dots only: one gemv_t per slab)
+        for s_, slab in enumerate(V.slabs):
+            kk = min(_CHUNK, V.count - s_ * _CHUNK)
+            if kk <= 0:
+                break
+            _lib.check(lib.sdmrg_gemv_t(kk, dim, slab.data_ptr(), dim, W.vec(k).data_ptr(),
+                                        coef[s_ * _CHUNK:].data_ptr(), stream))
+        col = coef[:V.count].cpu().numpy()
+        mat[:k + 1, k] = col
+        mat[k, :k + 1] = col          # rows from the column (H_eff is near-symmetric)
+
+    add(u)
+    theta = None
+    while True:
+        k = V.count
+        m = 0.5 * (mat[:k, :k] + mat[:k, :k].T)
+        evals, evecs = np.linalg.eigh(m)
+        theta, y = float(evals[0]), evecs[:, 0]
+        V.combine(y, u, stream)
+        W.combine(y, hu, stream)
+        _axpby(-theta, u, 1.0, hu, stream)             # hu := H u - θ u (residual)
+        _nrm2(hu, scal[0:1], stream)
+        rn = float(scal[0].item())
+        if rn <= tol * (1.0 + abs(theta)):
+            _nrm2(u, scal[1:2], stream)
+            _lib.check(lib.sdmrg_scal_dev(dim, None, scal[1:2].data_ptr(), 1, u.data_ptr(), stream))
+            return LanczosResult(theta, u, iters, True)
+        if iters >= max_iter:
+            return LanczosResult(theta, u, iters, False)
+        _lib.check(lib.sdmrg_davidson_precond(dim, hu.data_ptr(), diag.data_ptr(), theta,
+                                              t.data_ptr(), stream))
+        if V.count >= max_space:
+            # collapse: restart from the Ritz vector (its H u is recomputed)
+            _nrm2(u, scal[1:2], stream)
+            _lib.check(lib.sdmrg_scal_dev(dim, None, scal[1:2].data_ptr(), 1, u.data_ptr(), stream))
+            V.clear()
+            W.clear()
+            mat[:] = 0.0
+            add(u)
+            continue
+        V.project_out(t, stream)
+        V.project_out(t, stream, norm_out=scal[1:2])
+        tn = float(scal[1].item())
+        if tn < 1e-14:
+            return LanczosResult(theta, u, iters, False)
+        _axpby(1.0 / tn, t, 0.0, t, stream)
+        add(t)

@@ -202,6 +202,17 @@ class DevicePlan:
         view = torch.as_tensor(_View(), device=self.device)
         return view, offs
 
+    def diagonal(self, out=None):
+        """The diagonal of H_eff over this rank's ψ sectors (device vector in
+        the to_vector layout; sdmrg_plan_diagonal) — the Davidson
+        preconditioner.  Sum over ranks for the full diagonal."""
+        if out is None:
+            out = torch.empty(self.psi_size, dtype=torch.float64, device=self.device)
+        with _on_device(self.device):
+            _lib.check(_lib.load().sdmrg_plan_diagonal(self._h, out.data_ptr(),
+                                                       _stream_handle(device=self.device)))
+        return out
+
     def block_layout(self, side):
         """offsets[nops, nsec] of the operator blocks this plan holds in its
         padded arena for side 'l' / 'r' (-1: not held — blocks no ψ sector of

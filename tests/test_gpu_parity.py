@@ -443,3 +443,23 @@ def test_krylov_project_multislab():
     assert torch.allclose(coef, ref_c, rtol=1e-12, atol=1e-9)
     assert torch.allclose(w, ref_w, rtol=1e-10, atol=1e-9)
     assert abs(nrm.item() - ref_w.norm().item()) <= 1e-10 * ref_w.norm().item()
+
+
+def test_heff_diagonal_and_davidson(golden):
+    """sdmrg_plan_diagonal equals the diagonal of the oracle's H_eff (dense,
+    from unit vectors), and the diagonal-preconditioned device Davidson
+    reaches the reference Lanczos energy (dmrg.py:43) of the partition."""
+    from paper_2305_05581_b200.lanczos import davidson_ground, lanczos_ground
+    from paper_2305_05581_b200.plan import DevicePlan
+    name, pi = golden
+    plan = DevicePlan(pi)
+    n = plan.psi_size
+    groups = heff.build_groups(pi)
+    dense_diag = np.array([heff.apply_groups(pi, groups, np.eye(n)[j])[j] for j in range(n)])
+    d = plan.diagonal()
+    assert rel_err(d.cpu().numpy(), dense_diag) <= 1e-13
+    out = plan.empty_vector()
+    ref = lanczos_ground(lambda v: plan.apply(v, out), pi.meta["psi"], tol=1e-12, max_iter=300)
+    res = davidson_ground(lambda v: plan.apply(v, out), pi.meta["psi"], d, tol=1e-12, max_iter=300)
+    assert res.converged
+    assert abs(res.energy - ref.energy) <= 1e-10 * (1 + abs(ref.energy))
