@@ -268,7 +268,7 @@ def scale_point(n_orb, d, seed, peak, applies=3, n_elec=None):
     return res
 
 
-def sweep_point(n_orb, d, sweeps):
+def sweep_point(n_orb, d, sweeps, eigensolver="lanczos"):
     """sec/sweep of the closed-loop device DMRG (paper_2305_05581_b200.driver:
     native factorization, device block stores, composites, H_eff·psi plans,
     device Lanczos, renormalization, prediction) on the configs[0] model
@@ -280,7 +280,8 @@ def sweep_point(n_orb, d, sweeps):
     from paper_2305_05581_b200 import driver as drv
     from paper_2305_05581_b200 import model as M
     mm = M.Model(M.random_integrals(n_orb, 16, scale=0.2, core=0.3))
-    sch = drv.SweepSchedule(n_sweeps=sweeps, d=d, lanczos_tol=1e-10, lanczos_max_iter=300)
+    sch = drv.SweepSchedule(n_sweeps=sweeps, d=d, lanczos_tol=1e-10, lanczos_max_iter=300,
+                            eigensolver=eigensolver)
     t0 = time.perf_counter()
     st = drv.warmup(mm, sch, seed=42)
     torch.cuda.synchronize()
@@ -302,9 +303,10 @@ def sweep_point(n_orb, d, sweeps):
            for k in ("table_s", "aux_s", "plan_s", "lanczos_s", "renorm_s", "predict_s")}
     return {"workload": f"closed-loop two-site DMRG, random-integral L={n_orb}, U(1)xU(1), "
                         f"D={d} (BASELINE configs[0])",
-            "L": n_orb, "D": d, "sweeps": sweeps, "sec_per_sweep": per,
+            "L": n_orb, "D": d, "sweeps": sweeps, "eigensolver": eigensolver,
+            "sec_per_sweep": per,
             "warmup_s": round(warm, 3), "iterations_per_sweep": len(recs) // max(sweeps, 1),
-            "lanczos_iterations": sum(r.lanczos_iterations for r in recs),
+            "eigensolver_applies": sum(r.lanczos_iterations for r in recs),
             "breakdown_s_per_sweep": brk,
             "sweep_final_energy": recs[-1].energy if recs else None,
             "store_offloads": st.left.offloads + st.right.offloads}
@@ -559,9 +561,11 @@ def run_b200(args):
             v = [int(x) for x in item.split(":")]
             scale.append(scale_point(v[0], v[1], args.seed, peak,
                                      n_elec=v[2] if len(v) > 2 else None))
-    sweep = None
+    sweep = sweep_dav = None
     if world == 1 and args.sweep:
         sweep = sweep_point(*[int(x) for x in args.sweep.split(":")])
+        # the same sweep with the device Davidson (north-star eigensolver)
+        sweep_dav = sweep_point(*[int(x) for x in args.sweep.split(":")], eigensolver="davidson")
 
     value = exec_total / (ms * 1e-3) / 1e12
     dom = 1 if phase_ms[1] >= phase_ms[2] else 2   # the tensor-bound engine phases
@@ -624,6 +628,7 @@ def run_b200(args):
         "e2e": e2e,
         "krylov": krylov,
         "sweep": sweep,
+        "sweep_davidson": sweep_dav,
         "gpu_launches": int(launches),
         "clocks": clk,
     }

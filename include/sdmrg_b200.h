@@ -251,7 +251,7 @@ int sdmrg_gemv_n(int k, int64_t n, const double* v, int64_t ldv,
 int sdmrg_krylov_project(int nslabs, const double* const* slabs, int slab_rows, int k, int64_t n,
                          double* w, double* coef_dev, double* norm_dev, void* stream);
 /* Davidson correction vector with the diagonal preconditioner of H_eff
- * (sdmrg_plan_diagonal): t = r / (theta - diag), |theta - diag| >= 1e-8. */
+ * (sdmrg_plan_diagonal): t = r / (theta - diag), |theta - diag| >= 1e-3. */
 int sdmrg_davidson_precond(int64_t n, const double* r, const double* diag, double theta,
                            double* t, void* stream);
 int sdmrg_scal_dev(int64_t n, const double* num_dev, const double* den_dev,

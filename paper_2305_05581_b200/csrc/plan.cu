@@ -44,11 +44,12 @@ namespace {
 // Phase-2 σ blocks that span more than one 64 x 64 tile go to the 128 x 128
 // big-tile engine instance (engine_big.cu), whose CTA loads each shared
 // row / column operand panel once for all its quadrants.  SDMRG_BIG: 0 off;
-// 1 (default) σ blocks of 65..128 x 65..128; 2 also wider / taller blocks
-// (max(q, r) > 64, min(q, r) > 32) in <= 128 x 128 tiles.
+// 1 σ blocks of 65..128 x 65..128; 2 (default) also wider / taller blocks
+// (max(q, r) > 64, min(q, r) > 32) in <= 128 x 128 tiles (r2o: L=50 D=4096
+// 290 / 297 / 311 ms for 2 / 1 / 0).
 int big_tiles_mode() {
   const char* e = getenv("SDMRG_BIG");
-  return e ? std::atoi(e) : 1;
+  return e ? std::atoi(e) : 2;
 }
 bool big_tiles_enabled() { return big_tiles_mode() > 0; }
 inline bool big_problem(int q, int r) {

@@ -259,14 +259,16 @@ int sdmrg_krylov_project(int nslabs, const double* const* slabs, int slab_rows, 
 }
 
 // Davidson correction with the diagonal preconditioner:
-// t[j] = r[j] / (theta - diag[j]), |theta - diag[j]| floored at 1e-8
+// t[j] = r[j] / (theta - diag[j]), |theta - diag[j]| floored at 1e-3 (a
+// tiny floor lets the few diagonal entries nearest θ dominate the
+// correction and steer the search space off the ground state)
 __global__ void davidson_precond_kernel(int64_t n, const double* __restrict__ r,
                                         const double* __restrict__ diag, double theta,
                                         double* __restrict__ t) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double den = theta - diag[i];
-    if (fabs(den) < 1e-8) den = den < 0.0 ? -1e-8 : 1e-8;
+    if (fabs(den) < 1e-3) den = den < 0.0 ? -1e-3 : 1e-3;
     t[i] = r[i] / den;
   }
 }
