@@ -574,7 +574,7 @@ def run_b200(args):
     names = ["combine_kernel (phase 0: Lsum = sum s L)", "seg_gemm_kernel<0,1> (phase 1: T = A R^T)",
              ("seg_gemm_kernel<0,0> + fused_heff_kernel (phase 2: sigma += Lsum T; fused "
               "small-sector sigma problems)" if st.get("fused_outs") else
-              "seg_gemm_kernel<0,0> (phase 2: sigma += Lsum T)"),
+              "seg_gemm_kernel<0,0> 64x64 + sdmrg_big 128x128 (phase 2: sigma += Lsum T)"),
              "combine_kernel (phase 3: split-K partials into sigma)"]
     if dom in (0, 3):
         achieved = phase_bytes[dom] / (phase_ms[dom] * 1e-3) / 1e9
