@@ -53,6 +53,8 @@ def parse():
                     help="comma list of L:D[:electrons] workloads also timed at N=1 "
                          "(configs[1] L=30 D=2048 and the north-star CAS(113,76) D=4096 by "
                          "default; reported under 'scale_points'); empty to skip")
+    ap.add_argument("--sweep-davidson", action="store_true",
+                    help="also time the sweep with the diagonal-preconditioned Davidson")
     ap.add_argument("--sweep", default="16:256:1",
                     help="L:D:sweeps of the closed-loop device DMRG timed at N=1 (BASELINE "
                          "configs[0]: L=16 D=256; warm-up + SWEEPS timed sweeps, "
@@ -564,8 +566,10 @@ def run_b200(args):
     sweep = sweep_dav = None
     if world == 1 and args.sweep:
         sweep = sweep_point(*[int(x) for x in args.sweep.split(":")])
-        # the same sweep with the device Davidson (north-star eigensolver)
-        sweep_dav = sweep_point(*[int(x) for x in args.sweep.split(":")], eigensolver="davidson")
+        if args.sweep_davidson:
+            # the same sweep with the device Davidson (opt-in eigensolver)
+            sweep_dav = sweep_point(*[int(x) for x in args.sweep.split(":")],
+                                    eigensolver="davidson")
 
     value = exec_total / (ms * 1e-3) / 1e12
     dom = 1 if phase_ms[1] >= phase_ms[2] else 2   # the tensor-bound engine phases

@@ -1035,8 +1035,12 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     const double granule = std::max(
         total_cost / (double(d->dry_run ? 1 : engine_grid(false, false)) * split_factor()) + 1.0,
         split_min());
+    // big tiles: one CTA per SM, a granule per SDMRG_BIG_SPLIT (default as
+    // the 64-tile instance) of its share
+    const char* bse = getenv("SDMRG_BIG_SPLIT");
+    const double bsplit = bse ? std::max(1.0, std::atof(bse)) : split_factor();
     const double bgranule = std::max(
-        total_bcost / (double(d->dry_run ? 148 : sdmrg_internal_big_grid()) * split_factor()) + 1.0,
+        total_bcost / (double(d->dry_run ? 148 : sdmrg_internal_big_grid()) * bsplit) + 1.0,
         split_min());
     ch.host2big.cap = 128;
     const double fgranule =

@@ -158,28 +158,3 @@ def test_store_offload_is_transparent(monkeypatch):
     for a, b in zip(off.records, base.records):
         assert abs(a.energy - b.energy) <= 1e-12
 
-
-def test_closed_loop_davidson_matches_reference_L8_D32():
-    """The closed loop with the diagonal-preconditioned Davidson (north-star
-    eigensolver; the reference runs Lanczos): wherever the reference's
-    Lanczos converged, the Davidson energy agrees within 1e-8 Eh, up to the
-    first degenerate cut; and it needs fewer H_eff applications in total."""
-    from paper_2305_05581_b200 import driver as drv
-    from paper_2305_05581_b200 import model as M
-    hdr, ref = _load_record("sweep_record_L8_D32.jsonl")
-    mm = M.Model(M.random_integrals(hdr["L"], hdr["model_seed"], scale=0.2, core=0.3))
-    sch = drv.SweepSchedule(n_sweeps=hdr["sweeps"], d=hdr["D"], lanczos_tol=hdr["lanczos_tol"],
-                            lanczos_max_iter=hdr["lanczos_max_iter"], eigensolver="davidson")
-    st = drv.warmup(mm, sch, seed=hdr["run_seed"])
-    drv.run_sweeps(st, sch)
-    compared = 0
-    for a, b in zip(st.records, ref):
-        assert (a.sweep, a.position, a.direction) == (b["sweep"], b["position"], b["direction"])
-        if b["converged"]:
-            assert abs(a.energy - b["energy"]) <= E_TOL, (a.position, a.energy, b["energy"])
-            compared += 1
-        if a.timing["tie_at_cut"]:
-            break
-    assert compared >= 1
-    assert sum(r.lanczos_iterations for r in st.records[:len(ref)]) < \
-        sum(b["lanczos_iterations"] for b in ref)
