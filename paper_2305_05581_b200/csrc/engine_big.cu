@@ -18,7 +18,7 @@
 
 namespace {
 
-template <bool ONE>
+template <bool TB, bool ONE>
 int big_grid() {
   static std::mutex mu;
   static std::map<int, int> grids;
@@ -29,39 +29,41 @@ int big_grid() {
   if (it != grids.end()) return it->second;
   int sms = 0, per = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  auto* k = sdmrg_big::seg_gemm_kernel<false, false, true, ONE>;
+  auto* k = sdmrg_big::seg_gemm_kernel<false, TB, true, ONE>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       sdmrg_big::smem_bytes<false, false>());
+                       sdmrg_big::smem_bytes<false, TB>());
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, sdmrg_big::THREADS,
-                                                sdmrg_big::smem_bytes<false, false>());
+                                                sdmrg_big::smem_bytes<false, TB>());
   grids[dev] = sms * std::max(per, 1);
   return grids[dev];
 }
 
+template <bool TB, bool ONE>
+void launch(const sdmrg_big::TileRec* t, int ntiles, const sdmrg_big::Seg* sg, int* counter,
+            const sdmrg_big::Bases& b, cudaStream_t st) {
+  const int grid = std::min(big_grid<TB, ONE>(), ntiles);
+  sdmrg_big::seg_gemm_kernel<false, TB, true, ONE>
+      <<<grid, sdmrg_big::THREADS, sdmrg_big::smem_bytes<false, TB>(), st>>>(t, ntiles, sg, counter,
+                                                                            b);
+}
+
 }  // namespace
 
-// Launch the big-tile phase-2 instance (BULK operands, TA = TB = false)
-// over an uploaded tile / segment list; tiles must be <= 128 x 128.
+// Launch the big-tile instance (BULK operands, TA = false; trans_b: the
+// phase-1 form T = A B^T, else phase 2's C += A B) over an uploaded tile /
+// segment list; tiles must be <= 128 x 128.
 extern "C" int sdmrg_internal_launch_big(const void* tiles, int ntiles, const void* segs,
                                          int* counter, const void* bases, void* stream,
-                                         int one_body) {
+                                         int one_body, int trans_b) {
   if (ntiles <= 0) return 0;
   const auto& b = *static_cast<const sdmrg_big::Bases*>(bases);
   const auto* t = static_cast<const sdmrg_big::TileRec*>(tiles);
   const auto* sg = static_cast<const sdmrg_big::Seg*>(segs);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (one_body) {
-    const int grid = std::min(big_grid<true>(), ntiles);
-    sdmrg_big::seg_gemm_kernel<false, false, true, true>
-        <<<grid, sdmrg_big::THREADS, sdmrg_big::smem_bytes<false, false>(), st>>>(t, ntiles, sg,
-                                                                                 counter, b);
-  } else {
-    const int grid = std::min(big_grid<false>(), ntiles);
-    sdmrg_big::seg_gemm_kernel<false, false, true, false>
-        <<<grid, sdmrg_big::THREADS, sdmrg_big::smem_bytes<false, false>(), st>>>(t, ntiles, sg,
-                                                                                  counter, b);
-  }
+  if (trans_b) launch<true, false>(t, ntiles, sg, counter, b, st);
+  else if (one_body) launch<false, true>(t, ntiles, sg, counter, b, st);
+  else launch<false, false>(t, ntiles, sg, counter, b, st);
   return static_cast<int>(cudaGetLastError());
 }
 
-extern "C" int sdmrg_internal_big_grid() { return big_grid<false>(); }
+extern "C" int sdmrg_internal_big_grid() { return big_grid<false, false>(); }

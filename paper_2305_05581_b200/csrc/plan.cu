@@ -36,7 +36,7 @@ using namespace sdmrg;
 
 extern "C" int sdmrg_internal_launch_big(const void* tiles, int ntiles, const void* segs,
                                          int* counter, const void* bases, void* stream,
-                                         int one_body);
+                                         int one_body, int trans_b);
 extern "C" int sdmrg_internal_big_grid();
 
 namespace {
@@ -185,6 +185,8 @@ struct Chunk {
   DeviceBatch p1, p2;
   GemmBatch host2big;      // phase 2, σ blocks of 65..128 x 65..128 (engine_big.cu)
   DeviceBatch p2big;
+  GemmBatch host1big;      // phase 1, ψ keys of 65..128 rows (engine_big.cu)
+  DeviceBatch p1big;
   bool p2big_one_body = false;
   FusedBatch fused;        // small-sector σ problems on the fused kernel (fused.cuh)
   CombList comb0;          // phase 0: pre-summed left operators
@@ -869,6 +871,14 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     }
     for (int64_t x = 0; x < nkc; ++x) ws_key[x + 1] += ws_key[x];
     std::vector<GemmBatch> p1key(nkc);
+    // phase-1 products of ψ keys with 65..128 rows on the big-tile instance
+    // (row siblings share the right-operator panel; SDMRG_BIG_P1=0: off)
+    const bool big1 = big_tiles_enabled() && !(getenv("SDMRG_BIG_P1") && getenv("SDMRG_BIG_P1")[0] == '0');
+    if (big1)
+      for (int64_t i = i0; i < i1; ++i) {
+        const int m = d->dim_l[keys[i].jl];
+        if (m > 64 && m <= 128) p1key[i - i0].cap = 128;
+      }
     int64_t f1 = 0, np1 = 0;
 #pragma omp parallel for schedule(dynamic, 8) reduction(+ : f1, np1)
     for (int64_t i = i0; i < i1; ++i) {
@@ -909,7 +919,11 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
         }
       }
     }
-    for (auto& gb : p1key) ch.host1.append(std::move(gb));
+    ch.host1big.cap = 128;
+    for (auto& gb : p1key) {
+      if (gb.cap == 128) ch.host1big.append(std::move(gb));
+      else ch.host1.append(std::move(gb));
+    }
     p1key.clear();
     int64_t ws = ws_key[nkc];
     exec_flops += f1;
@@ -1105,6 +1119,9 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       ch.bytes3 += 8LL * (co.term_end - co.term_begin + 1) * qr;
     }
     ch.host1.finalize_tiles(0, getenv("SDMRG_P1_BY_PROBLEM") != nullptr);
+    ch.host1big.finalize_tiles(0, false);
+    tiles += (int64_t)ch.host1big.tiles.size();
+    segments += (int64_t)ch.host1big.segs.size();
     ch.host2.finalize_tiles(p2_octaves(), getenv("SDMRG_P2_BY_PROBLEM") != nullptr);
     ch.p2_one_body = use_one_body(ch.host2);
     ch.host2big.finalize_tiles(0, false);
@@ -1211,7 +1228,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
                              "memset workspace");
   }
   if (!rc && !plan->chunks.empty())
-    rc = cuda_check(cudaMalloc(&plan->counters, sizeof(int) * 4 * plan->chunks.size()),
+    rc = cuda_check(cudaMalloc(&plan->counters, sizeof(int) * 5 * plan->chunks.size()),
                     "cudaMalloc counters");
   int64_t max_slots = 0;
   for (auto& ch : plan->chunks) {
@@ -1219,6 +1236,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     rc = ch.host1.upload(&ch.p1, 0);
     if (!rc) rc = ch.host2.upload(&ch.p2, 0);
     if (!rc) rc = ch.host2big.upload(&ch.p2big, 0);
+    if (!rc) rc = ch.host1big.upload(&ch.p1big, 0);
     if (!rc) rc = ch.fused.upload();
     max_slots = std::max(max_slots, ch.p2.nslots);
     for (CombList* cl : {&ch.comb0, &ch.comb3}) {
@@ -1233,6 +1251,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     ch.host1 = GemmBatch();
     ch.host2 = GemmBatch();
     ch.host2big = GemmBatch();
+    ch.host1big = GemmBatch();
   }
   if (!rc && SDMRG_LOCKSTEP > 0 && max_slots > 0 && !getenv("SDMRG_NO_LOCK"))
     rc = cuda_check(cudaMalloc(&plan->progress, sizeof(int) * max_slots), "cudaMalloc progress");
@@ -1258,7 +1277,7 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   st.workspace_doubles = ws_max;
   int64_t kernels = 0;
   for (auto& ch : plan->chunks)
-    kernels += (ch.comb0.ntasks > 0) + (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0) + (ch.p2big.ntiles > 0) + (ch.fused.ntiles > 0) +
+    kernels += (ch.comb0.ntasks > 0) + (ch.p1.ntiles > 0) + (ch.p2.ntiles > 0) + (ch.p2big.ntiles > 0) + (ch.p1big.ntiles > 0) + (ch.fused.ntiles > 0) +
                (ch.comb3.ntasks > 0);
   st.kernels_per_apply = kernels;
   st.algo_bytes = static_cast<int64_t>(algo_bytes);
@@ -1354,7 +1373,7 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (rc) return rc;
   }
   if (plan->chunks.empty()) return SDMRG_OK;
-  rc = cuda_check(cudaMemsetAsync(plan->counters, 0, sizeof(int) * 4 * plan->chunks.size(), stream),
+  rc = cuda_check(cudaMemsetAsync(plan->counters, 0, sizeof(int) * 5 * plan->chunks.size(), stream),
                   "memset counters");
   if (rc) return rc;
   if (plan->psi_copy.n > 0) {
@@ -1397,8 +1416,16 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (plan->timing) cudaEventRecord(ch.ev[1], s0);
     if (fork) cudaEventRecord(plan->join, plan->side);
     if (plan->timing) cudaEventRecord(ch.ev[2], stream);
-    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 4 * c, stream, true);
+    rc = launch_engine(false, true, ch.p1, bases, plan->counters + 5 * c, stream, true);
     if (rc) return rc;
+    if (ch.p1big.ntiles > 0) {
+      rc = cuda_check(static_cast<cudaError_t>(sdmrg_internal_launch_big(
+                          ch.p1big.tiles, static_cast<int>(ch.p1big.ntiles), ch.p1big.segs,
+                          plan->counters + 5 * c + 4, &bases, stream, 0, 1)),
+                      "big-tile phase-1 launch");
+      count_launch();
+      if (rc) return rc;
+    }
     if (plan->timing) cudaEventRecord(ch.ev[3], stream);
     if (fork) cudaStreamWaitEvent(stream, plan->join, 0);
     if (plan->timing) cudaEventRecord(ch.ev[4], stream);
@@ -1409,15 +1436,15 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
       if (rc) return rc;
       b2.p[kMaxBases - 1] = reinterpret_cast<double*>(plan->progress);
     }
-    rc = launch_engine(false, false, ch.p2, b2, plan->counters + 4 * c + 1, stream, true,
+    rc = launch_engine(false, false, ch.p2, b2, plan->counters + 5 * c + 1, stream, true,
                        ch.p2_one_body);
     if (rc) return rc;
-    rc = launch_fused(ch.fused, bases, plan->counters + 4 * c + 2, stream);
+    rc = launch_fused(ch.fused, bases, plan->counters + 5 * c + 2, stream);
     if (rc) return rc;
     if (ch.p2big.ntiles > 0) {
       rc = cuda_check(static_cast<cudaError_t>(sdmrg_internal_launch_big(
                           ch.p2big.tiles, static_cast<int>(ch.p2big.ntiles), ch.p2big.segs,
-                          plan->counters + 4 * c + 3, &bases, stream, ch.p2big_one_body)),
+                          plan->counters + 5 * c + 3, &bases, stream, ch.p2big_one_body, 0)),
                       "big-tile engine launch");
       count_launch();
     }
@@ -1485,6 +1512,7 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
     ch.p1.release();
     ch.p2.release();
     ch.p2big.release();
+    ch.p1big.release();
     ch.fused.release();
     ch.comb0.release();
     ch.comb3.release();
