@@ -87,15 +87,13 @@ struct Tile {        // host only
 };
 // Device form of a tile: the problem fields folded in, so the producer needs
 // one dependent load (tile -> segment) instead of two.
-struct TileRec {     // 48 B
+struct TileRec {     // 40 B
   uint64_t c;        // handle of C(0,0) of the problem
   int32_t ldc, beta;
   int32_t seg_begin, seg_end;
   int32_t row0, col0;
   int16_t tm, tn;
   int32_t colw;      // column-tile width of the problem (stage-tiled B)
-  int32_t sib_slot;  // SDMRG_LOCKSTEP: first progress slot of the problem's tiles
-  int16_t nsib, sib; // tiles of the problem, this tile's index among them
 };
 struct Seg {         // 40 B
   uint64_t a;        // handle of opA(0,0)
@@ -119,13 +117,10 @@ struct Seg {         // 40 B
 #define SDMRG_BIG 0
 #endif
 #ifndef SDMRG_STAGES
-#define SDMRG_STAGES (SDMRG_BIG ? 5 : (SDMRG_WIDE ? 4 : 3))
+#define SDMRG_STAGES (SDMRG_BIG ? 5 : 3)
 #endif
 #ifndef SDMRG_TILE
 #define SDMRG_TILE 64
-#endif
-#ifndef SDMRG_DB
-#define SDMRG_DB 0
 #endif
 #ifndef SDMRG_STCS
 #define SDMRG_STCS 0
@@ -134,9 +129,6 @@ struct Seg {         // 40 B
 // number of 8-row (8-column) blocks, so the four DMMA warps stay balanced
 #ifndef SDMRG_ROTATE
 #define SDMRG_ROTATE 1
-#endif
-#ifndef SDMRG_LOCKSTEP
-#define SDMRG_LOCKSTEP 0
 #endif
 #ifndef SDMRG_GRID_ADAPT
 #define SDMRG_GRID_ADAPT 1
@@ -156,29 +148,13 @@ template <bool TB>
 __host__ __device__ constexpr bool grid_adapt() {
   return SDMRG_GRID_ADAPT && SDMRG_TILE == 64 && TB;
 }
-// K order inside a stage (same for both operands, so any bijection is
-// exact): DMMA k4 step ks, thread column lc reads stage k
-//   kperm(ks, lc) = 8 (ks >> 1) + 2 lc + (ks & 1)
-// so a thread's k pairs (2lc, 2lc+1) and (8+2lc, 9+2lc) feed steps (0,1) and
-// (2,3): one LDS.128 per K-contiguous fragment pair instead of two LDS.64.
-// Off by default: parity-exact but measured 2% slower (96.1 vs 94.2 ms).
-#ifndef SDMRG_LDS128
-#define SDMRG_LDS128 0
-#endif
 #ifndef SDMRG_MINB
-#define SDMRG_MINB (SDMRG_BIG ? 1 : ((SDMRG_TILE > 64 || SDMRG_WIDE) ? 2 : 4))
+#define SDMRG_MINB (SDMRG_BIG ? 1 : 4)
 #endif
-// SDMRG_WIDE: 64 x 128 tiles, 8 DMMA warps (2 x 4 grid of <= 32 x 32 warp
-// tiles) per CTA, 2 CTAs per SM — the same 16 DMMA warps per SM as the
-// default, with half the A-panel re-reads between column tiles.
-#ifndef SDMRG_WIDE
-#define SDMRG_WIDE 0
-#endif
-constexpr int BM = SDMRG_TILE, BN = SDMRG_WIDE ? 2 * SDMRG_TILE : SDMRG_TILE, BK = 16;
+constexpr int BM = SDMRG_TILE, BN = SDMRG_TILE, BK = 16;
 constexpr int STAGES = SDMRG_STAGES;
-constexpr int MAXB = BM / 16;                    // 8x8 blocks per warp and dimension
-static_assert(BM == 64 || BM == 96 || (SDMRG_BIG && BM == 128), "tile edge 64, 96 (or 128 big)");
-constexpr int WGRID_R = SDMRG_BIG ? 4 : 2, WGRID_C = (SDMRG_WIDE || SDMRG_BIG) ? 4 : 2,
+static_assert(BM == 64 || (SDMRG_BIG && BM == 128), "tile edge 64 (128: the big instance)");
+constexpr int WGRID_R = SDMRG_BIG ? 4 : 2, WGRID_C = SDMRG_BIG ? 4 : 2,
               CONSUMERS = WGRID_R * WGRID_C;
 // SDMRG_PRODUCERS=2: one producer warp per operand (A loader leads the tile
 // queue, the B loader follows through shared memory and a named barrier)
@@ -209,41 +185,14 @@ __host__ __device__ constexpr int stage_elems() { return a_elems<TA>() + b_elems
 // Per-stage metadata written by the producer's lane 0.
 struct StageMeta {
   double* c;         // tile origin in C (first stage of a tile)
-  double scale;      // != 1: some k4 step of the stage is scaled
-  double kscale[4];  // scale of each k4 step (packed stages: one per segment piece)
+  double scale;      // != 1: the stage's segment is scaled
   int32_t nks;       // k4 steps in this stage (0: no K, or kEnd)
   int32_t flags;
   int32_t ldc, beta;
   int16_t tm, tn;
   int32_t pad;
 };
-constexpr int kFirst = 1, kLast = 2, kEnd = 4, kPacked = 8;
-// Segment packing (aligned path): a stage's 16 k rows are filled from as many
-// consecutive segments of the tile as fit, each starting on a k4 boundary
-// with its own scale per k4 step — short segments (small sectors: K = a few
-// states) no longer cost one ring stage each (L=30 D=512: 1.5x fewer phase-2
-// stages, D=2048: 1.09x).
-#ifndef SDMRG_PACK
-#define SDMRG_PACK 0
-#endif
-#ifndef SDMRG_ROUND
-#define SDMRG_ROUND 0
-#endif
-#ifndef SDMRG_PACK_P2
-#define SDMRG_PACK_P2 0
-#endif
-// Measured (profiles/r1_notes.md): packing made phase 2 13-17% slower (and
-// 1.8x slower at D=512) even with uniform-scale stages only (SDMRG_PACK=2),
-// and phase 1 (one segment per tile) neutral — off by default; build
-// variants SDMRG_PACK=1/2 (+ SDMRG_PACK_P2=1 for the phase-2 instance) are
-// parity-tested.
-template <bool TB>
-__host__ __device__ constexpr bool pack_path() {
-  return SDMRG_PACK && (TB || SDMRG_PACK_P2);
-}
-static_assert(!(SDMRG_PACK && (SDMRG_LDS128 || SDMRG_DB)), "packing needs the natural k order");
-static_assert(!(SDMRG_SWZ && (SDMRG_PACK || SDMRG_LDS128 || SDMRG_DB)), "swizzle: natural-order bodies only");
-
+constexpr int kFirst = 1, kLast = 2, kEnd = 4;
 template <bool TA, bool TB>
 __host__ __device__ constexpr int smem_bytes() {
   return STAGES * stage_elems<TA, TB>() * 8 + STAGES * (int)sizeof(StageMeta) + 2 * STAGES * 8 +
@@ -308,13 +257,7 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
 
 // k4 steps needed to cover stage k < krem (every stage k >= krem is zero in
 // both operands: the loaders zero-fill the tail of every stage).
-__host__ __device__ constexpr int steps_for(int krem) {
-#if SDMRG_LDS128
-  return krem <= 1 ? 1 : krem <= 8 ? 2 : krem <= 9 ? 3 : 4;
-#else
-  return (krem + 3) >> 2;
-#endif
-}
+__host__ __device__ constexpr int steps_for(int krem) { return (krem + 3) >> 2; }
 
 __device__ __forceinline__ void lds128(uint32_t addr, double& x, double& y) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(addr));
@@ -360,50 +303,8 @@ __device__ __forceinline__ void consume_tile(const Ring& ring, int& stage, uint3
     const int flags = m.flags;
     const int nks = m.nks;
     const double scale = m.scale;
-    // per-k4-step scale (packed stages; an LDS issued with the step's
-    // fragment loads); the whole-stage scale otherwise
-    const uint32_t ksc_addr = static_cast<uint32_t>(__cvta_generic_to_shared(&m.kscale[0]));
-    auto ksc = [&](int ks) { return pack_path<TB>() && SDMRG_PACK == 1 ? lds64(ksc_addr + 8 * ks) : scale; };
     const uint32_t a0 = ring.smem + stage * STAGE_B + a_off;
     const uint32_t b0 = ring.smem + stage * STAGE_B + b_off;
-#if SDMRG_DB
-static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
-    if (MB > 0 && NB > 0 && nks > 0) {
-      // fragments of k4 step ks+1 loaded (and scaled) around the DMMAs of ks
-      const bool scaled = __double_as_longlong(scale) != 0x3FF0000000000000LL;
-      double af[2][MB > 0 ? MB : 1], bf[2][NB > 0 ? NB : 1];
-      auto load = [&](int ks, int buf) {
-#pragma unroll
-        for (int i = 0; i < MB; ++i) af[buf][i] = lds64(a0 + ks * A_KS + i * A_I);
-#pragma unroll
-        for (int j = 0; j < NB; ++j) bf[buf][j] = lds64(b0 + ks * B_KS + j * B_J);
-      };
-      auto rescale = [&](int buf) {
-        if (NB <= MB) {
-#pragma unroll
-          for (int j = 0; j < NB; ++j) bf[buf][j] *= scale;
-        } else {
-#pragma unroll
-          for (int i = 0; i < MB; ++i) af[buf][i] *= scale;
-        }
-      };
-      load(0, 0);
-      if (scaled) rescale(0);
-#pragma unroll
-      for (int ks = 0; ks < BK / 4; ++ks) {
-        if (ks < nks) {
-          const int cur = ks & 1, nxt = cur ^ 1;
-          const bool more = ks + 1 < BK / 4 && ks + 1 < nks;
-          if (more) load(ks + 1, nxt);
-#pragma unroll
-          for (int i = 0; i < MB; ++i)
-#pragma unroll
-            for (int j = 0; j < NB; ++j) dmma(acc[i][j], af[cur][i], bf[cur][j]);
-          if (more && scaled) rescale(nxt);
-        }
-      }
-    }
-#else
     if (MB > 0 && NB > 0) {
 #ifdef SDMRG_EXP_NOSCALE
       const bool scaled = false;
@@ -417,53 +318,6 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
       // scales, and a DMUL takes FP64-pipe slots from the DMMAs)
       auto body = [&](auto scaled_t) {
         constexpr bool SCALED = decltype(scaled_t)::value;
-#if SDMRG_LDS128
-        // K-contiguous operands: fragments of steps (2h, 2h+1) in one LDS.128
-        // at stage k = 8h + 2lc (a0/b0 point at k = 2lc); M/N-contiguous
-        // operands: one LDS.64 per step at stage row kperm(ks, lc)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (2 * h < nks) {
-            double ap[MB > 0 ? MB : 1][2], bp[NB > 0 ? NB : 1][2];
-#pragma unroll
-            for (int i = 0; i < MB; ++i) {
-              if (!TA) lds128(a0 + h * 64 + i * A_I, ap[i][0], ap[i][1]);
-              else {
-                ap[i][0] = lds64(a0 + (8 * h) * NC_LD_A * 8 + i * A_I);
-                ap[i][1] = lds64(a0 + (8 * h + 1) * NC_LD_A * 8 + i * A_I);
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < NB; ++j) {
-              if (TB) lds128(b0 + h * 64 + j * B_J, bp[j][0], bp[j][1]);
-              else {
-                bp[j][0] = lds64(b0 + (8 * h) * NC_LD_B * 8 + j * B_J);
-                bp[j][1] = lds64(b0 + (8 * h + 1) * NC_LD_B * 8 + j * B_J);
-              }
-            }
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              if (2 * h + e < nks) {
-                if (SCALED) {
-                  if (NB <= MB) {
-#pragma unroll
-                    for (int j = 0; j < NB; ++j) bp[j][e] *= scale;
-                  } else {
-#pragma unroll
-                    for (int i = 0; i < MB; ++i) ap[i][e] *= scale;
-                  }
-                }
-#ifndef SDMRG_EXP_NOMMA
-#pragma unroll
-                for (int i = 0; i < MB; ++i)
-#pragma unroll
-                  for (int j = 0; j < NB; ++j) dmma(acc[i][j], ap[i][e], bp[j][e]);
-#endif
-              }
-            }
-          }
-        }
-#else
 #pragma unroll
         for (int ks = 0; ks < BK / 4; ++ks) {
           if (ks < nks) {
@@ -473,7 +327,7 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
 #pragma unroll
             for (int j = 0; j < NB; ++j) bf[j] = lds64(b0 + koff_b(ks) + j * B_J);
             if (SCALED) {
-              const double sk = ksc(ks);
+              const double sk = scale;
               if (NB <= MB) {
 #pragma unroll
                 for (int j = 0; j < NB; ++j) bf[j] *= sk;
@@ -490,7 +344,6 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
 #endif
           }
         }
-#endif
       };
       if constexpr (ONE) {
         body(std::true_type{});  // unit scales multiply too: half the code
@@ -499,7 +352,6 @@ static_assert(!SDMRG_LDS128, "double buffering assumes the natural k order");
         else body(std::false_type{});
       }
     }
-#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(ring.empty0 + 8 * stage);
     if (++stage == STAGES) {
@@ -565,18 +417,6 @@ __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring&
                                                  uint32_t& phase, uint32_t a_off, uint32_t b_off,
                                                  double* c, int ldc, int beta, int row_lim,
                                                  int col_lim, int lane) {
-  if constexpr (ONE && SDMRG_ROUND) {
-    switch (mblk * 8 + nblk) {
-      SDMRG_TILE_CASE(4, 4) SDMRG_TILE_CASE(4, 2) SDMRG_TILE_CASE(4, 1)
-      SDMRG_TILE_CASE(2, 4) SDMRG_TILE_CASE(2, 2) SDMRG_TILE_CASE(2, 1)
-      SDMRG_TILE_CASE(1, 4) SDMRG_TILE_CASE(1, 2) SDMRG_TILE_CASE(1, 1)
-      default:
-        consume_tile<TA, TB, 0, 0, ONE>(ring, stage, phase, a_off, b_off, c, ldc, beta, row_lim,
-                                        col_lim, lane);
-        break;
-    }
-    return;
-  }
   if constexpr (grid_adapt<TB>()) {
     if (mblk > 4 || nblk > 4) {  // 1 x 4 / 4 x 1 warp grids of odd-block tiles
       switch (mblk * 8 + nblk) {
@@ -588,13 +428,6 @@ __device__ __forceinline__ void consume_dispatch(int mblk, int nblk, const Ring&
     }
   }
   switch (mblk * 8 + nblk) {
-#if SDMRG_TILE > 64 && !SDMRG_BIG
-    SDMRG_TILE_CASE(6, 6) SDMRG_TILE_CASE(6, 5) SDMRG_TILE_CASE(5, 6) SDMRG_TILE_CASE(5, 5)
-    SDMRG_TILE_CASE(6, 4) SDMRG_TILE_CASE(6, 3) SDMRG_TILE_CASE(6, 2) SDMRG_TILE_CASE(6, 1)
-    SDMRG_TILE_CASE(5, 4) SDMRG_TILE_CASE(5, 3) SDMRG_TILE_CASE(5, 2) SDMRG_TILE_CASE(5, 1)
-    SDMRG_TILE_CASE(4, 6) SDMRG_TILE_CASE(4, 5) SDMRG_TILE_CASE(3, 6) SDMRG_TILE_CASE(3, 5)
-    SDMRG_TILE_CASE(2, 6) SDMRG_TILE_CASE(2, 5) SDMRG_TILE_CASE(1, 6) SDMRG_TILE_CASE(1, 5)
-#endif
     SDMRG_TILE_CASE(4, 4) SDMRG_TILE_CASE(4, 3) SDMRG_TILE_CASE(4, 2) SDMRG_TILE_CASE(4, 1)
     SDMRG_TILE_CASE(3, 4) SDMRG_TILE_CASE(3, 3) SDMRG_TILE_CASE(3, 2) SDMRG_TILE_CASE(3, 1)
     SDMRG_TILE_CASE(2, 4) SDMRG_TILE_CASE(2, 3) SDMRG_TILE_CASE(2, 2) SDMRG_TILE_CASE(2, 1)
@@ -668,39 +501,9 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const double* gmem, i
 __device__ __forceinline__ void cp_async16_full(uint32_t saddr, const double* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
 }
-// SDMRG_L2HINT: L2 eviction priority per operand (createpolicy +
-// cp.async ...L2::cache_hint): the streamed-once operand (phase 2: T,
-// written by phase 1 and read by ~1.1 groups) evict-first, the re-used one
-// (the operator blocks, each read by many products) evict-last.
-#ifndef SDMRG_L2HINT
-#define SDMRG_L2HINT 0
-#endif
-__device__ __forceinline__ uint64_t l2_policy(bool keep) {
-  uint64_t p;
-  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void cp_async16_hint(uint32_t saddr, const double* gmem, int src_bytes,
-                                                uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(saddr),
-               "l"(gmem), "r"(src_bytes), "l"(pol));
-}
-template <bool HINT>
-__device__ __forceinline__ void cp16(uint32_t saddr, const double* gmem, int src_bytes, uint64_t pol) {
-  if (HINT) cp_async16_hint(saddr, gmem, src_bytes, pol);
-  else cp_async16(saddr, gmem, src_bytes);
-}
-template <bool HINT>
-__device__ __forceinline__ void cp16_full(uint32_t saddr, const double* gmem, uint64_t pol) {
-  if (HINT) cp_async16_hint(saddr, gmem, 16, pol);
-  else cp_async16_full(saddr, gmem);
-}
-
-template <bool KCONTIG, int NC_LD, int CAP, bool HINT = false>
+template <bool KCONTIG, int NC_LD, int CAP>
 __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const double* src, int ld,
-                                                     int extent, int krem, int lane,
-                                                     uint64_t pol = 0) {
+                                                     int extent, int krem, int lane) {
   if (KCONTIG) {
     const int k = 2 * (lane & 7), r0 = lane >> 3;
     const double* p = src + (int64_t)r0 * ld + k;
@@ -709,13 +512,13 @@ __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const doubl
     const int nrow = (extent - r0 + 3) >> 2;
     if (k + 1 < krem) {
 #pragma unroll 4
-      for (int i = 0; i < nrow; ++i) cp16_full<HINT>(s0 + i * (4 * KC_LD * 8), p + (int64_t)(4 * i) * ld, pol);
+      for (int i = 0; i < nrow; ++i) cp_async16_full(s0 + i * (4 * KC_LD * 8), p + (int64_t)(4 * i) * ld);
     } else {
       const int bytes = k < krem ? 8 : 0;
       const double* q = k < krem ? p : src;
       const int64_t step = k < krem ? 4 * (int64_t)ld : 0;
 #pragma unroll 4
-      for (int i = 0; i < nrow; ++i) cp16<HINT>(s0 + i * (4 * KC_LD * 8), q + i * step, bytes, pol);
+      for (int i = 0; i < nrow; ++i) cp_async16(s0 + i * (4 * KC_LD * 8), q + i * step, bytes);
     }
   } else {
 #pragma unroll
@@ -726,84 +529,15 @@ __device__ __forceinline__ void load_operand_aligned(uint32_t sbase, const doubl
         const uint32_t s0 = sbase + c * 8;
         if (krem >= BK) {
 #pragma unroll
-          for (int k = 0; k < BK; ++k) cp16_full<HINT>(s0 + k * (NC_LD * 8), p + (int64_t)k * ld, pol);
+          for (int k = 0; k < BK; ++k) cp_async16_full(s0 + k * (NC_LD * 8), p + (int64_t)k * ld);
         } else {
 #pragma unroll
           for (int k = 0; k < BK; ++k)
-            cp16<HINT>(s0 + k * (NC_LD * 8), k < krem ? p + (int64_t)k * ld : src,
-                       k < krem ? 16 : 0, pol);
+            cp_async16(s0 + k * (NC_LD * 8), k < krem ? p + (int64_t)k * ld : src,
+                       k < krem ? 16 : 0);
         }
       }
     }
-  }
-}
-
-// Packed-stage variant: stage k rows [kb, kb + len) (kb, len multiples of 4)
-// from source k rows [0, len), rows >= valid zero-filled; the stage's other
-// rows belong to other segments and are not touched.
-template <bool KCONTIG, int NC_LD, int CAP>
-__device__ __forceinline__ void load_operand_range(uint32_t sbase, const double* src, int ld,
-                                                   int extent, int kb, int len, int valid,
-                                                   int lane) {
-  if (KCONTIG) {
-    const int k = 2 * (lane & 7), r0 = lane >> 3;
-    if (k < kb || k >= kb + len) return;
-    const int kk = k - kb;
-    const int bytes = kk + 1 < valid ? 16 : (kk < valid ? 8 : 0);
-    const double* p = bytes ? src + (int64_t)r0 * ld + kk : src;
-    const int64_t step = bytes ? 4 * (int64_t)ld : 0;
-    const uint32_t s0 = sbase + (r0 * KC_LD + k) * 8;
-    const int nrow = (extent - r0 + 3) >> 2;
-#pragma unroll 4
-    for (int i = 0; i < nrow; ++i) cp_async16(s0 + i * (4 * KC_LD * 8), p + i * step, bytes);
-  } else {
-#pragma unroll
-    for (int j = 0; j < (CAP + 63) / 64; ++j) {
-      const int c = 2 * lane + 64 * j;
-      if (c < extent) {
-        const double* p = src + c;
-        const uint32_t s0 = sbase + c * 8;
-#pragma unroll
-        for (int k = 0; k < BK; ++k) {
-          const int kk = k - kb;
-          if (kk >= 0 && kk < len)
-            cp_async16(s0 + k * (NC_LD * 8), kk < valid ? p + (int64_t)kk * ld : src,
-                       kk < valid ? 16 : 0);
-        }
-      }
-    }
-  }
-}
-
-// L2 prefetch of one contiguous element range with a single bulk (TMA-unit)
-// prefetch: the range is widened to 16-byte alignment.
-__device__ __forceinline__ void bulk_prefetch_l2(const double* first, const double* last) {
-  const uint64_t lo = reinterpret_cast<uint64_t>(first) & ~uint64_t(15);
-  const uint64_t hi = (reinterpret_cast<uint64_t>(last) + 8 + 15) & ~uint64_t(15);
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(lo), "r"((uint32_t)(hi - lo))
-               : "memory");
-}
-
-// Prefetch both operand panels of segment sg for the tile (row0, col0, tm,
-// tn) into L2: each panel of a row-major sector block is one address range.
-template <bool TA, bool TB>
-__device__ __forceinline__ void prefetch_segment(const Seg& sg, const TileRec& tr,
-                                                 double* const* sbases) {
-  const double* a = sbases[sg.a >> kHandleShift] + (sg.a & kHandleMask);
-  const double* b = sbases[sg.b >> kHandleShift] + (sg.b & kHandleMask);
-  if (TA) {
-    const double* p = a + tr.row0;
-    bulk_prefetch_l2(p, p + (int64_t)(sg.k - 1) * sg.lda + tr.tm - 1);
-  } else {
-    const double* p = a + (int64_t)tr.row0 * sg.lda;
-    bulk_prefetch_l2(p, p + (int64_t)(tr.tm - 1) * sg.lda + sg.k - 1);
-  }
-  if (TB) {
-    const double* p = b + (int64_t)tr.col0 * sg.ldb;
-    bulk_prefetch_l2(p, p + (int64_t)(tr.tn - 1) * sg.ldb + sg.k - 1);
-  } else {
-    const double* p = b + tr.col0;
-    bulk_prefetch_l2(p, p + (int64_t)(sg.k - 1) * sg.ldb + tr.tn - 1);
   }
 }
 
@@ -824,8 +558,6 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
       m.nks = nks;
       m.scale = scale;
       m.flags = flags;
-      if (!(flags & kPacked))
-        m.kscale[0] = m.kscale[1] = m.kscale[2] = m.kscale[3] = scale;
       if (flags & kFirst) {
         m.c = cptr;
         m.ldc = tr.ldc;
@@ -850,14 +582,6 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
   };
   int stage = 0;
   uint32_t phase = 0;
-  // phase 1 (TB): A = ψ (small, L2-resident), B = right operator blocks
-  // (re-used by every ψ key of their sector); phase 2: A = operator blocks /
-  // pre-sums (re-used), B = T (streamed)
-  uint64_t pol_a = 0, pol_b = 0;
-  if (SDMRG_L2HINT) {
-    pol_a = l2_policy(true);
-    pol_b = l2_policy(TB);
-  }
   // Tile queue with two tiles of lookahead: the index of tile i+2 is claimed
   // while tile i streams and its descriptor is loaded at the end of tile i, so
   // neither the atomic nor the dependent descriptor load sits on the path
@@ -895,47 +619,11 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
       }
       if (next < ntiles && nrec.seg_begin < nrec.seg_end) sn = segs[nrec.seg_begin];
     }
-    // SDMRG_LOCKSTEP: the tiles of one σ problem read the same operand
-    // panels (row siblings the same A rows, column siblings the same B
-    // columns); a producer more than SDMRG_LOCKSTEP segments ahead of a
-    // started, unfinished sibling waits for it, so the shared panels are
-    // read while still in L2.  The slowest sibling never waits: no deadlock,
-    // and the data flow is untouched (timing only).
-    volatile int* prog = reinterpret_cast<volatile int*>(sbases[kMaxBases - 1]);
-    const bool lock = SDMRG_LOCKSTEP > 0 && prog != nullptr && cur.nsib > 1;
-    if (lock && lane == 0) prog[cur.sib_slot + cur.sib] = 1;
     bool first = true;
-    int kfill = 0;           // packed rows in the open stage (multiple of 4)
-    double open_scale = 1.0; // SDMRG_PACK == 2: the open stage's (uniform) scale
-    bool unit = true;        // every k4 step of the open stage unscaled
     for (int s = cur.seg_begin; s < cur.seg_end; ++s) {
-      if (lock) {
-        const int k = s - cur.seg_begin;
-        if (lane == 0) {
-          prog[cur.sib_slot + cur.sib] = k + 1;
-          for (int j = 0; j < cur.nsib; ++j) {
-            if (j == cur.sib) continue;
-            int v = prog[cur.sib_slot + j];
-            while (v >= 1 && v < (1 << 30) && v - 1 < k - SDMRG_LOCKSTEP) {
-              __nanosleep(256);
-              v = prog[cur.sib_slot + j];
-            }
-          }
-        }
-        __syncwarp();
-      }
       const Seg sg = sn;
-      if (s + 1 < cur.seg_end) {
-        sn = segs[s + 1];
-#ifdef SDMRG_L2_PREFETCH
-        if (lane == 0) prefetch_segment<TA, TB>(sn, cur, sbases);
-#endif
-      } else if (next < ntiles && nrec.seg_begin < nrec.seg_end) {
-        sn = segs[nrec.seg_begin];
-#ifdef SDMRG_L2_PREFETCH
-        if (lane == 0) prefetch_segment<TA, TB>(sn, nrec, sbases);
-#endif
-      }
+      if (s + 1 < cur.seg_end) sn = segs[s + 1];
+      else if (next < ntiles && nrec.seg_begin < nrec.seg_end) sn = segs[nrec.seg_begin];
       const double* a = sbases[sg.a >> kHandleShift] + (sg.a & kHandleMask);
       const double* b = sbases[sg.b >> kHandleShift] + (sg.b & kHandleMask);
       // operand origins at this tile: A rows row0.., B cols col0..
@@ -943,84 +631,6 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
       const bool btiled = !TB && BULK && sg.btile > 0;
       if (btiled) b += (int64_t)(cur.col0 / cur.colw) * sg.btile * NC_LD_B;
       else b += TB ? (int64_t)cur.col0 * sg.ldb : cur.col0;
-      if (pack_path<TB>() && BULK && !btiled) {
-        if (SDMRG_PACK == 2 && kfill > 0 &&
-            __double_as_longlong(sg.scale) != __double_as_longlong(open_scale)) {
-          // uniform-scale stages: close the open one before a new scale
-          meta_write(stage, kfill >> 2, open_scale, (first ? kFirst : 0), cur, cptr);
-          __syncwarp();
-          mbar_arrive_cp_async(ring.full0 + 8 * stage);
-          if (lane == 0 && leader) mbar_arrive(ring.full0 + 8 * stage);
-          first = false;
-          kfill = 0;
-          unit = true;
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        open_scale = sg.scale;
-        for (int k0 = 0; k0 < sg.k;) {
-          if (kfill == 0) mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
-          const uint32_t sa = ring.smem + stage * STAGE_B;
-          const uint32_t sb = sa + A_EL * 8;
-          const int valid = min(BK - kfill, sg.k - k0);
-          const int len = min(BK - kfill, (sg.k - k0 + 3) & ~3);
-          const double* asrc = TA ? a + (int64_t)k0 * sg.lda : a + k0;
-          const double* bsrc = TB ? b + k0 : b + (int64_t)k0 * sg.ldb;
-#ifndef SDMRG_EXP_NOLOAD
-          if (kfill == 0 && len == BK) {
-            if (load_a) load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, valid, lane);
-            if (load_b) load_operand_aligned<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, valid, lane);
-          } else {
-            if (load_a)
-              load_operand_range<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, kfill, len, valid, lane);
-            if (load_b)
-              load_operand_range<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, kfill, len, valid, lane);
-          }
-#endif
-          if (lane == 0 && leader) {
-            StageMeta& m = ring.meta[stage];
-            for (int q = kfill >> 2; q < (kfill + len) >> 2; ++q) m.kscale[q] = sg.scale;
-          }
-          unit = unit && __double_as_longlong(sg.scale) == 0x3FF0000000000000LL;
-          kfill += len;
-          k0 += len;
-          const bool last = (s + 1 == cur.seg_end) && k0 >= sg.k;
-          if (kfill == BK || last) {
-            meta_write(stage, kfill >> 2, SDMRG_PACK == 2 ? open_scale : (unit ? 1.0 : 2.0),
-                       (SDMRG_PACK == 2 ? 0 : kPacked) | (first ? kFirst : 0) | (last ? kLast : 0),
-                       cur, cptr);
-            __syncwarp();
-            const uint32_t full = ring.full0 + 8 * stage;
-            mbar_arrive_cp_async(full);
-            if (lane == 0 && leader) mbar_arrive(full);
-            first = false;
-            kfill = 0;
-            unit = true;
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-        }
-        continue;
-      }
-      if (kfill > 0) {
-        // a stage-tiled segment after packed ones: close the open stage
-        meta_write(stage, kfill >> 2, SDMRG_PACK == 2 ? open_scale : (unit ? 1.0 : 2.0),
-                   (SDMRG_PACK == 2 ? 0 : kPacked) | (first ? kFirst : 0), cur, cptr);
-        __syncwarp();
-        mbar_arrive_cp_async(ring.full0 + 8 * stage);
-        if (lane == 0 && leader) mbar_arrive(ring.full0 + 8 * stage);
-        first = false;
-        kfill = 0;
-        unit = true;
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
       for (int k0 = 0; k0 < sg.k; k0 += BK) {
         const int krem = min(BK, sg.k - k0);
         mbar_wait(ring.empty0 + 8 * stage, phase ^ 1);
@@ -1045,11 +655,8 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
           }
           if (load_a) load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
         } else if (BULK) {
-          constexpr bool H = SDMRG_L2HINT != 0;
-          if (load_a)
-            load_operand_aligned<!TA, NC_LD_A, BM, H>(sa, asrc, sg.lda, cur.tm, krem, lane, pol_a);
-          if (load_b)
-            load_operand_aligned<TB, NC_LD_B, BN, H>(sb, bsrc, sg.ldb, cur.tn, krem, lane, pol_b);
+          if (load_a) load_operand_aligned<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
+          if (load_b) load_operand_aligned<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
         } else {
           if (load_a) load_operand_async<!TA, NC_LD_A, BM>(sa, asrc, sg.lda, cur.tm, krem, lane);
           if (load_b) load_operand_async<TB, NC_LD_B, BN>(sb, bsrc, sg.ldb, cur.tn, krem, lane);
@@ -1065,7 +672,6 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
         }
       }
     }
-    if (lock && lane == 0) prog[cur.sib_slot + cur.sib] = 1 << 30;  // finished
     t2 = __shfl_sync(0xffffffffu, t2, 0);
     share(t2, 0);
     TileRec n2{};
@@ -1085,8 +691,6 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
 // launcher selects it per batch.
 #if SDMRG_BIG
 #define SDMRG_KERNEL_BOUNDS __launch_bounds__(THREADS, 1)
-#elif SDMRG_TILE > 64
-#define SDMRG_KERNEL_BOUNDS __maxnreg__(200)
 #else
 #define SDMRG_KERNEL_BOUNDS __launch_bounds__(THREADS, SDMRG_MINB)
 #endif
@@ -1177,21 +781,13 @@ seg_gemm_kernel(const TileRec* __restrict__ tiles, int ntiles, const Seg* __rest
       wc0 = 8 * (wc * nbase + min(wc, nextra));
     }
     // fragment origin: stage k = lc (natural order) or 2 lc (kperm)
-    const int kf = SDMRG_LDS128 ? 2 * lc : lc;
+    const int kf = lc;
     const uint32_t a_off = TA ? (kf * NC_LD_A + wr0 + lr) * 8 : ((wr0 + lr) * KC_LD + kf) * 8;
     const uint32_t b_off =
         A_EL * 8 + (TB ? ((wc0 + lr) * KC_LD + kf) * 8 : (kf * NC_LD_B + wc0 + lr) * 8);
     double* c = m.c + (int64_t)(wr0 + lr) * m.ldc + wc0 + 2 * lc;
-    if constexpr (ONE && SDMRG_ROUND) {
-      // 3 -> 4 blocks (the extra block's DMMAs are discarded: its stores are
-      // cut at the warp's own extent): 9 shape bodies instead of 16
-      const int re = min(tm - wr0, 8 * mblk) - lr, ce = min(tn - wc0, 8 * nblk) - 2 * lc;
-      consume_dispatch<TA, TB, ONE>(mblk == 3 ? 4 : mblk, nblk == 3 ? 4 : nblk, ring, stage, phase,
-                                    a_off, b_off, c, m.ldc, m.beta, re, ce, lane);
-    } else {
-      consume_dispatch<TA, TB, ONE>(mblk, nblk, ring, stage, phase, a_off, b_off, c, m.ldc,
-                                    m.beta, tm - wr0 - lr, tn - wc0 - 2 * lc, lane);
-    }
+    consume_dispatch<TA, TB, ONE>(mblk, nblk, ring, stage, phase, a_off, b_off, c, m.ldc,
+                                  m.beta, tm - wr0 - lr, tn - wc0 - 2 * lc, lane);
   }
 }
 

@@ -77,7 +77,7 @@ int sdmrg_grouped_gemm(int trans_a, int trans_b, int64_t nprob, const int64_t* c
   for (size_t i = 0; i < gb.tiles.size(); ++i) {
     const Tile& t = gb.tiles[i];
     const Prob& p = gb.probs[t.prob];
-    recs[i] = TileRec{p.c, p.ldc, p.beta, p.seg_begin, p.seg_end, t.row0, t.col0, t.tm, t.tn, t.colw, 0, 1, 0};
+    recs[i] = TileRec{p.c, p.ldc, p.beta, p.seg_begin, p.seg_end, t.row0, t.col0, t.tm, t.tn, t.colw};
   }
   DeviceBatch db;
   int* counter = nullptr;

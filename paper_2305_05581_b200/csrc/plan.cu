@@ -241,7 +241,6 @@ struct sdmrg_plan {
   cudaEvent_t fork = nullptr, join = nullptr;
   sdmrg_plan_stats stats{};
   int64_t fused_outs = 0;          // σ problems on the fused kernel
-  int* progress = nullptr;         // phase-2 sibling progress slots (SDMRG_LOCKSTEP)
   std::vector<DiagKey> diag_keys;  // H_eff diagonal work (this rank's ψ keys)
   std::vector<DiagMem> diag_mems;
   double shard_balance = 1.0;      // mean / max rank load (world > 1)
@@ -1230,7 +1229,6 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
   if (!rc && !plan->chunks.empty())
     rc = cuda_check(cudaMalloc(&plan->counters, sizeof(int) * 5 * plan->chunks.size()),
                     "cudaMalloc counters");
-  int64_t max_slots = 0;
   for (auto& ch : plan->chunks) {
     if (rc) break;
     rc = ch.host1.upload(&ch.p1, 0);
@@ -1238,7 +1236,6 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     if (!rc) rc = ch.host2big.upload(&ch.p2big, 0);
     if (!rc) rc = ch.host1big.upload(&ch.p1big, 0);
     if (!rc) rc = ch.fused.upload();
-    max_slots = std::max(max_slots, ch.p2.nslots);
     for (CombList* cl : {&ch.comb0, &ch.comb3}) {
       if (!rc) rc = upload_vec(cl->tasks, &cl->d_tasks);
       if (!rc) rc = upload_vec(cl->outs, &cl->d_outs);
@@ -1253,8 +1250,6 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     ch.host2big = GemmBatch();
     ch.host1big = GemmBatch();
   }
-  if (!rc && SDMRG_LOCKSTEP > 0 && max_slots > 0 && !getenv("SDMRG_NO_LOCK"))
-    rc = cuda_check(cudaMalloc(&plan->progress, sizeof(int) * max_slots), "cudaMalloc progress");
   if (rc) {
     sdmrg_plan_destroy(plan);
     return rc;
@@ -1429,14 +1424,7 @@ int sdmrg_plan_apply(sdmrg_plan* plan, const double* psi, double* sigma, int acc
     if (plan->timing) cudaEventRecord(ch.ev[3], stream);
     if (fork) cudaStreamWaitEvent(stream, plan->join, 0);
     if (plan->timing) cudaEventRecord(ch.ev[4], stream);
-    Bases b2 = bases;
-    if (plan->progress && ch.p2.nslots > 0) {
-      rc = cuda_check(cudaMemsetAsync(plan->progress, 0, sizeof(int) * ch.p2.nslots, stream),
-                      "memset progress");
-      if (rc) return rc;
-      b2.p[kMaxBases - 1] = reinterpret_cast<double*>(plan->progress);
-    }
-    rc = launch_engine(false, false, ch.p2, b2, plan->counters + 5 * c + 1, stream, true,
+    rc = launch_engine(false, false, ch.p2, bases, plan->counters + 5 * c + 1, stream, true,
                        ch.p2_one_body);
     if (rc) return rc;
     rc = launch_fused(ch.fused, bases, plan->counters + 5 * c + 2, stream);
@@ -1531,7 +1519,6 @@ int sdmrg_plan_destroy(sdmrg_plan* plan) {
   if (plan->join) cudaEventDestroy(plan->join);
   if (plan->side) cudaStreamDestroy(plan->side);
   if (plan->counters) cudaFree(plan->counters);
-  if (plan->progress) cudaFree(plan->progress);
   delete plan;
   return SDMRG_OK;
 }

@@ -190,25 +190,12 @@ int GemmBatch::upload(DeviceBatch* out, cudaStream_t stream) const {
   int rc;
   if (!tiles.empty()) {
     std::vector<TileRec> recs(tiles.size());
-    // sibling groups (SDMRG_LOCKSTEP): one progress slot per tile of every
-    // multi-tile problem, slots of a problem contiguous
-    std::vector<int32_t> ntile(probs.size(), 0), slot0(probs.size(), -1), seen(probs.size(), 0);
-    for (const Tile& t : tiles) ++ntile[t.prob];
-    int32_t nslot = 0;
-    for (size_t p = 0; p < probs.size(); ++p)
-      if (ntile[p] > 1) {
-        slot0[p] = nslot;
-        nslot += ntile[p];
-      }
     for (size_t i = 0; i < tiles.size(); ++i) {
       const Tile& t = tiles[i];
       const Prob& p = probs[t.prob];
       recs[i] = TileRec{p.c, p.ldc, p.beta, p.seg_begin, p.seg_end, t.row0, t.col0, t.tm, t.tn,
-                        t.colw, std::max(slot0[t.prob], 0),
-                        static_cast<int16_t>(ntile[t.prob] > 1 && ntile[t.prob] < 32000 ? ntile[t.prob] : 1),
-                        static_cast<int16_t>(seen[t.prob]++)};
+                        t.colw};
     }
-    out->nslots = nslot;
     if ((rc = cuda_check(cudaMalloc(&out->tiles, recs.size() * sizeof(TileRec)), "cudaMalloc tiles")))
       return rc;
     if ((rc = cuda_check(cudaMemcpy(out->tiles, recs.data(), recs.size() * sizeof(TileRec),

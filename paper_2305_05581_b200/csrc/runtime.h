@@ -24,7 +24,6 @@ struct DeviceBatch {
   TileRec* tiles = nullptr;
   Seg* segs = nullptr;
   int64_t ntiles = 0, nprobs = 0, nsegs = 0;
-  int64_t nslots = 0;   // sibling progress slots (SDMRG_LOCKSTEP)
   void release();
 };
 
