@@ -1,8 +1,7 @@
 #!/bin/bash
 # Round-end GPU pass: smoke, the whole -m gpu suite, the bench line and the
 # reference arm, the ncu launch list of the bench command, one full ncu
-# capture of each engine phase at the bench workload (L=50 D=4096), the
-# cuobjdump SASS opcode summary of the shipped library.  tools/gpu_final.sh TAG
+# capture of each engine kernel at the bench workload (L=50 D=4096).  tools/gpu_final.sh TAG
 TAG=${1:-final}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
@@ -15,8 +14,8 @@ timeout 1200 python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/ben
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --scale "" --sweep "" > $OUT/bench_under_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_gemm_kernel -s 2 -c 1 \
-    -o $OUT/prof_p1 python tools/prof_apply.py 50 4096 2 > $OUT/ncu_p1.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_gemm_kernel -s 3 -c 1 \
-    -o $OUT/prof_p2 python tools/prof_apply.py 50 4096 2 > $OUT/ncu_p2.log 2>&1
+for k in "p1:sdmrg::seg_gemm_kernel<.bool.0, .bool.1" "p2small:sdmrg::seg_gemm_kernel<.bool.0, .bool.0" "p2big:sdmrg_big::seg_gemm_kernel<.bool.0, .bool.0"; do
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k regex:"${k#*:}" -s 0 -c 1 -o $OUT/prof_${k%%:*} python tools/prof_apply.py 50 4096 1 > $OUT/ncu_${k%%:*}.log 2>&1
+done
 ls -la $OUT
