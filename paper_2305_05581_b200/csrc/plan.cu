@@ -872,11 +872,14 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
     std::vector<GemmBatch> p1key(nkc);
     // phase-1 products of ψ keys with 65..128 rows on the big-tile instance
     // (row siblings share the right-operator panel; SDMRG_BIG_P1=0: off)
-    const bool big1 = big_tiles_enabled() && !(getenv("SDMRG_BIG_P1") && getenv("SDMRG_BIG_P1")[0] == '0');
-    if (big1)
+    // SDMRG_BIG_P1: 0 off, 1 (default) m in 65..128, 2 every m > 64 (rows
+    // cut into <= 128-row tiles)
+    const char* bp1 = getenv("SDMRG_BIG_P1");
+    const int big1 = big_tiles_enabled() ? (bp1 ? std::atoi(bp1) : 1) : 0;
+    if (big1 > 0)
       for (int64_t i = i0; i < i1; ++i) {
         const int m = d->dim_l[keys[i].jl];
-        if (m > 64 && m <= 128) p1key[i - i0].cap = 128;
+        if (m > 64 && (m <= 128 || big1 == 2)) p1key[i - i0].cap = 128;
       }
     int64_t f1 = 0, np1 = 0;
 #pragma omp parallel for schedule(dynamic, 8) reduction(+ : f1, np1)
