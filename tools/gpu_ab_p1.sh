@@ -2,7 +2,7 @@
 TAG=${1:-abp1}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-timeout 600 python -m pytest tests/test_gpu_bench_parity.py -q -x -k "L30_D2048" > $OUT/pytest.log 2>&1; echo "rc=$?" >> $OUT/pytest.log
+SDMRG_BIG_P1=2 timeout 600 python -m pytest tests/test_gpu_bench_parity.py -q -x -k "L30_D2048" > $OUT/pytest.log 2>&1; echo "rc=$?" >> $OUT/pytest.log
 for order in "1 2" "2 1"; do
   for v in $order; do
     for cfg in "30 2048" "30 4096" "50 4096"; do
