@@ -130,9 +130,6 @@ struct Seg {         // 40 B
 #ifndef SDMRG_ROTATE
 #define SDMRG_ROTATE 1
 #endif
-#ifndef SDMRG_SEG_PREFETCH
-#define SDMRG_SEG_PREFETCH 0
-#endif
 #ifndef SDMRG_GRID_ADAPT
 #define SDMRG_GRID_ADAPT 1
 #endif
@@ -627,12 +624,6 @@ __device__ __forceinline__ void produce(const Ring& ring, const TileRec* __restr
       const Seg sg = sn;
       if (s + 1 < cur.seg_end) sn = segs[s + 1];
       else if (next < ntiles && nrec.seg_begin < nrec.seg_end) sn = segs[nrec.seg_begin];
-#if SDMRG_SEG_PREFETCH
-      // small tiles: a segment lasts ~3 short stages, about one descriptor
-      // load latency — pull the descriptors a few segments ahead into L2
-      if (lane == 0 && s + SDMRG_SEG_PREFETCH < cur.seg_end)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(segs + s + SDMRG_SEG_PREFETCH));
-#endif
       const double* a = sbases[sg.a >> kHandleShift] + (sg.a & kHandleMask);
       const double* b = sbases[sg.b >> kHandleShift] + (sg.b & kHandleMask);
       // operand origins at this tile: A rows row0.., B cols col0..
