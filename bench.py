@@ -4,10 +4,13 @@
 Workload (BASELINE.json configs[2], the largest single-GPU config): the
 middle two-site partition of an L=50 synthetic-integral CAS(50,50),
 U(1)xU(1) (the reference has no SU(2) layer), bond dimension D=4096 per
-block; configs[1] (L=30, D=2048) is timed as a scale point.  The operator
-table is the reference's own factorization of a random-integral Hamiltonian
-(fixture); block data are synthetic (seeded normal blocks on the sector
-structure, see paper_2305_05581_b200/workload.py).
+block.  Scale points at N=1: configs[1] (L=30, D=2048) and the north-star
+CAS(113,76) at D=4096 and D=8192.  The operator table is the reference's own
+factorization of a random-integral Hamiltonian (fixture; L=76 from the
+native factorization, checked bit-exact against the reference's tables);
+block data are synthetic (seeded normal blocks on the sector structure, see
+paper_2305_05581_b200/workload.py).  ``sweep``: warm-up + one timed sweep of
+the closed-loop device DMRG at configs[0] (L=16, D=256).
 
 One step = one full H_eff·ψ (σ = H_eff ψ, every operator-table row against
 every ψ sector).  ``value`` = FP64 FLOPs the engine executes / device time
@@ -16,9 +19,9 @@ the reference's FLOP count of the same product (blocks.py:575 plan.flops)
 / device time, a time-to-solution rate.  Operators (2 x 10 GB) exceed L2,
 so every step streams them from HBM (no flush needed).
 
-N>1 (torchrun): ψ sectors are sharded over ranks (balanced LPT), each rank
-computes its partial σ, NCCL all-reduce sums them: strong scaling of one
-H_eff·ψ.  ``--impl reference`` times the reference algorithm on the host
+N>1 (torchrun): ψ sectors are sharded over ranks (whole left sectors, LPT),
+each rank holds only the operator blocks its sectors read and computes its
+partial σ, NCCL all-reduce sums them: strong scaling of one H_eff·ψ.  ``--impl reference`` times the reference algorithm on the host
 (oracle port: numpy restatement of dmrg.py:107 apply_plan / sbmm4s Alg. 2,
 NumPy BLAS on all host cores) on a bounded sample of the same groups.
 """
