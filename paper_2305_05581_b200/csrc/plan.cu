@@ -1048,8 +1048,18 @@ int sdmrg_plan_build(const sdmrg_plan_desc* d, sdmrg_plan** out) {
       else if (big_on && big_problem(op.q, op.r)) total_bcost += double(op.q) * op.r * op.ksum;
       else total_cost += double(op.q) * op.r * op.ksum;
     }
+    // small-sector plans (every σ block one 64-tile: CAS(113,76) D=4096)
+    // balance better with a granule of 1/192 of a CTA's share (r2z: phase 2
+    // 137 vs 145 ms there; multi-tile plans keep 1/96)
+    bool all_small = true;
+    for (const OutProb& op : outs)
+      if (op.q > 64 || op.r > 64) {
+        all_small = false;
+        break;
+      }
+    const double sf = (all_small && !getenv("SDMRG_SPLIT")) ? 2.0 * split_factor() : split_factor();
     const double granule = std::max(
-        total_cost / (double(d->dry_run ? 1 : engine_grid(false, false)) * split_factor()) + 1.0,
+        total_cost / (double(d->dry_run ? 1 : engine_grid(false, false)) * sf) + 1.0,
         split_min());
     // big tiles: one CTA per SM, a granule per SDMRG_BIG_SPLIT (default as
     // the 64-tile instance) of its share
